@@ -1,0 +1,469 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 F_p polynomial-matrix product path (driver contract).
+
+Default workload: BASELINE.json configs[1] (cfg2): A, B 32x32 over
+p = 2013265921, entries of degree < 4096, 8192 evaluation points.  A step is
+one exact product C = A*B on device-resident inputs.  value = algorithmic
+modular multiplications per second (SURVEY.md 8(d) convention) for the
+whole job over all ranks; every rank runs its own product (independent units,
+no data-path collective: weak scaling).
+
+--impl reference runs the CPU restatement of the reference path
+(oracle/libfpm_oracle.so, "port") on the host cores instead.
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P31 = 2013265921
+P60 = (1 << 60) - 93
+METRIC = "F_p polmat-mul ms & Gmodmul/s, % roofline (NTT HBM, pointwise MMA); PM-Basis ms"
+
+CONFIGS = {
+    "cfg1": dict(kind="mul", p=P31, m=4, k=4, n=4, deg=1023),
+    "cfg2": dict(kind="mul", p=P31, m=32, k=32, n=32, deg=4095),
+    "cfg3": dict(kind="mul", p=P60, m=16, k=16, n=16, deg=2047),
+    "cfg4": dict(kind="pmbasis", p=P31, m=64, n=32, sigma=4096),
+    "cfg5": dict(kind="mul", p=P31, m=256, k=256, n=256, deg=2047),
+}
+CRT_PRIMES = [2130706433, 2113929217, 2013265921, 1811939329, 1711276033, 1224736769,
+              1107296257]
+
+
+def two_adicity(p):
+    k, m = 0, p - 1
+    while m % 2 == 0:
+        m //= 2
+        k += 1
+    return k
+
+
+def mul_plan(cfg):
+    """N, number of word primes r (1 = direct) for a product config."""
+    la = lb = cfg["deg"] + 1
+    need = la + lb - 1
+    logn = max(5, (need - 1).bit_length())
+    p = cfg["p"]
+    if p < (1 << 31) and two_adicity(p) >= logn:
+        return 1 << logn, 1
+    lg = (math.log2(cfg["k"]) + math.log2(min(la, lb)) + 2 * math.log2(p - 1) + 2)
+    have, r = 0.0, 0
+    for q in CRT_PRIMES:
+        if have > lg:
+            break
+        have += math.log2(q)
+        r += 1
+    return 1 << logn, r
+
+
+def mul_work(cfg):
+    """Algorithmic modmuls and per-stage algorithmic bytes."""
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    la = lb = cfg["deg"] + 1
+    lc = la + lb - 1
+    N, r = mul_plan(cfg)
+    logn = N.bit_length() - 1
+    ntt = (N // 2) * logn
+    modmul = r * ((m * k + k * n + m * n) * ntt + m * n * N + N * m * k * n)
+    eb = 4 if cfg["p"] < (1 << 31) else 8
+    bytes_ = {
+        "ntt_fwd_A": r * m * k * (eb * la + 4 * N),
+        "ntt_fwd_B": r * k * n * (eb * lb + 4 * N),
+        "pointwise": r * 4 * N * (m * k + k * n + m * n),
+        "ntt_inv": r * m * n * 4 * (N + lc),
+    }
+    if r > 1:
+        bytes_["crt"] = m * n * lc * (4 * r + 8)
+    return modmul, bytes_, N, r
+
+
+def pmbasis_work(cfg):
+    """Algorithmic modmul estimate of PM-Basis (tree ~13.9 G
+    + base ~7.1 G at cfg4), scaled by sigma * m^2 * n / (4096 * 64^2 * 32)."""
+    s = cfg["sigma"] / 4096.0 * (cfg["m"] / 64.0) ** 2 * (cfg["n"] / 32.0)
+    return int(21.0e9 * s)
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def read_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(cfg, device, seed):
+    import torch
+
+    from paper_1905_04356_b200 import dense
+
+    g = torch.Generator(device=device).manual_seed(seed)
+    p = cfg["p"]
+    dt = dense.torch_dtype(p)
+
+    def rnd(shape):
+        if p < (1 << 31):
+            return torch.randint(0, p, shape, generator=g, device=device, dtype=torch.int64).to(dt)
+        hi = torch.randint(0, 1 << 30, shape, generator=g, device=device, dtype=torch.int64)
+        lo = torch.randint(0, 1 << 30, shape, generator=g, device=device, dtype=torch.int64)
+        return ((hi << 30) | lo) % p
+
+    if cfg["kind"] == "mul":
+        L = cfg["deg"] + 1
+        return rnd((cfg["m"], cfg["k"], L)), rnd((cfg["k"], cfg["n"], L))
+    return (rnd((cfg["m"], cfg["n"], cfg["sigma"])),)
+
+
+def run_step(cfg, inputs, out=None):
+    from paper_1905_04356_b200 import dense
+
+    if cfg["kind"] == "mul":
+        return dense.pm_mul_dense(inputs[0], inputs[1], cfg["p"], out=out)
+    return dense.pmbasis_dense(inputs[0], cfg["sigma"], [0] * cfg["m"], cfg["p"])[0]
+
+
+def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
+    """Per-step CUDA-event time (ms list) with an L2 flush between steps."""
+    import torch
+
+    from paper_1905_04356_b200 import _lib
+
+    out = None
+    if cfg["kind"] == "mul":
+        out = run_step(cfg, inputs)
+    for _ in range(warmup):
+        run_step(cfg, inputs, out)
+    torch.cuda.synchronize()
+    times = []
+    stages = {}
+    n0 = _lib.launch_count()
+    for _ in range(steps):
+        flush.zero_()
+        if profile_h is not None:
+            _lib.profile(profile_h, True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run_step(cfg, inputs, out)
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        if profile_h is not None:
+            for name, ms in _lib.profile_records(profile_h):
+                stages.setdefault(name, []).append(ms)
+    launches = _lib.launch_count() - n0
+    if profile_h is not None:
+        _lib.profile(profile_h, False)
+    return times, stages, launches
+
+
+def e2e_mul(cfg, steps, warmup, seed):
+    """Same metric through the C ABI host entry (pinned host buffers)."""
+    import numpy as np
+    import torch
+
+    from paper_1905_04356_b200 import _lib, dense
+
+    p = cfg["p"]
+    A, B = make_inputs(cfg, "cuda", seed)
+    Ah = A.cpu().pin_memory()
+    Bh = B.cpu().pin_memory()
+    m, k, la = A.shape
+    _, n, lb = B.shape
+    lc = la + lb - 1
+    Ch = torch.empty((m, n, lc), dtype=A.dtype).pin_memory()
+    h = _lib.context()
+    L = _lib.lib()
+    eb = dense.elem_bytes_for(p)
+
+    def call():
+        _lib.check(L.fpm_polmat_mul_host(h, p, eb, Ah.data_ptr(), m, k, la, Bh.data_ptr(), n,
+                                         lb, Ch.data_ptr()), "fpm_polmat_mul_host")
+
+    for _ in range(warmup):
+        call()
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        call()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    med = ts[len(ts) // 2]
+    _ = np
+    return med, Ah.numel() * eb + Bh.numel() * eb, Ch.numel() * eb
+
+
+def cpu_baseline(cfg, budget_s=10.0, threads=None):
+    """Oracle port of the reference path on host cores (bounded sample)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    threads = threads or os.cpu_count() or 1
+    O.set_threads(threads)
+    p = cfg["p"]
+    rng = np.random.default_rng(1)
+    if cfg["kind"] == "mul":
+        L = cfg["deg"] + 1
+        A = rng.integers(0, p, size=(cfg["m"], cfg["k"], L), dtype=np.uint64)
+        B = rng.integers(0, p, size=(cfg["k"], cfg["n"], L), dtype=np.uint64)
+        work = mul_work(cfg)[0]
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            O.pm_mul(p, A, B)
+            reps += 1
+            if time.perf_counter() - t0 > budget_s or reps >= 3:
+                break
+        dt = (time.perf_counter() - t0) / reps
+        return {"value": work / dt / 1e9, "unit": "Gmodmul/s", "cores": threads,
+                "kind": "port", "seconds_per_step": dt,
+                "sample": f"{reps} full {cfg['m']}x{cfg['k']}x{cfg['n']} deg<{L} products "
+                          f"(oracle/libfpm_oracle.so, OpenMP {threads} threads)"}
+    raise ValueError("cpu baseline only for product configs")
+
+
+def reference_arm(args, cfg, rank):
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    import numpy as np
+
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    p = cfg["p"]
+    L = cfg["deg"] + 1
+    rng = np.random.default_rng(1)
+    A = rng.integers(0, p, size=(cfg["m"], cfg["k"], L), dtype=np.uint64)
+    B = rng.integers(0, p, size=(cfg["k"], cfg["n"], L), dtype=np.uint64)
+    for _ in range(min(args.warmup, 1)):
+        O.pm_mul(p, A, B)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.pm_mul(p, A, B)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    work = mul_work(cfg)[0]
+    val = work * args.steps / total / 1e9
+    line = {
+        "metric": METRIC, "value": val, "unit": "Gmodmul/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform in [0,p))",
+        "config": {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"}},
+        "cpu_baseline": {"value": val, "unit": "Gmodmul/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full products on host cores "
+                                   "(CPU restatement of polmat._pm_mul_ntt, oracle/)"},
+        "e2e": {"value": val, "unit": "Gmodmul/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def per_config_table(device):
+    """Short timing of every BASELINE config (ms, Gmodmul/s) for the report."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    out = {}
+    for name, cfg in CONFIGS.items():
+        try:
+            inputs = make_inputs(cfg, device, 100 + int(name[-1]))
+            steps, warm = (3, 1) if cfg["kind"] == "pmbasis" else (10, 3)
+            ts, _, _ = time_steps(cfg, inputs, steps, warm, flush)
+            ts.sort()
+            ms = ts[len(ts) // 2]
+            work = mul_work(cfg)[0] if cfg["kind"] == "mul" else pmbasis_work(cfg)
+            out[name] = {"ms": round(ms, 4), "Gmodmul_s": round(work / ms / 1e6, 2)}
+            del inputs
+        except Exception as exc:  # report, never hide
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip cpu_baseline / e2e / per-config table")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        line = reference_arm(args, cfg, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+
+    from paper_1905_04356_b200 import _lib
+
+    h = _lib.context(local)
+    inputs = make_inputs(cfg, device, 1000 + rank)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
+    clocks = Clocks(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times, stages, launches = time_steps(cfg, inputs, args.steps, args.warmup, flush,
+                                         profile_h=h)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = sum(times)
+    if dist is not None:
+        t = torch.tensor([total_ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_step = total_ms / args.steps
+    if cfg["kind"] == "mul":
+        work, sbytes, N, r = mul_work(cfg)
+    else:
+        work, sbytes, N, r = pmbasis_work(cfg), {}, None, None
+    value = world * work * args.steps / (total_ms * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Gmodmul/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32" if cfg["p"] < (1 << 31) else "u64",
+        "data": "synthetic (seeded uniform coefficients in [0,p), torch.Generator)",
+        "config": {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"},
+                   "N": N, "word_primes": r,
+                   "l2": "flushed: 256 MiB write between timed steps (outside events)",
+                   "parallelism": f"replicas x{world} (independent products per rank)"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    # roofline of the dominant kernel stage, CUDA events inside the timed region
+    if stages:
+        avg = {k: sum(v) / len(v) for k, v in stages.items()}
+        line["stages_ms"] = {k: round(v, 5) for k, v in avg.items()}
+        dom = max(avg, key=avg.get)
+        peak, peak_src = read_peaks()
+        if dom in sbytes:
+            ach = sbytes[dom] / (avg[dom] * 1e-3) / 1e9
+            traffic = read_traffic().get(args.config, {}).get(dom)
+            line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1),
+                                "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                                "traffic": traffic, "algorithmic_bytes": sbytes[dom],
+                                "peak_source": peak_src}
+    if rank == 0 and not args.no_extras and cfg["kind"] == "mul":
+        try:
+            med, bi, bo = e2e_mul(cfg, max(3, args.steps // 2), 2, 7)
+            line["e2e"] = {"value": round(work / med / 1e9, 3), "unit": "Gmodmul/s",
+                           "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+                           "ms_per_step": round(med * 1e3, 4),
+                           "path": "fpm_polmat_mul_host (C ABI, pinned host buffers)"}
+        except Exception as exc:
+            line["e2e"] = {"error": f"{type(exc).__name__}: {exc}"}
+        if world == 1:
+            try:
+                line["cpu_baseline"] = cpu_baseline(cfg)
+            except Exception as exc:
+                line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+            line["per_config"] = per_config_table(device)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/*
+ * fpmat_b200.h -- C ABI of libfpm_b200.so, the B200 (sm_100a) drop-in for the
+ * F_p polynomial-matrix multiply and PM-Basis path of the reference `fpmat`
+ * package (/root/reference/pkg/src/fpmat, arXiv:1905.04356 / PML).
+ *
+ * The reference has no FFI of its own: its boundary is the set of Python
+ * callables below.  Every entry point here replaces
+ * exactly one of them; INTEGRATION.md shows the ctypes binding a maintainer
+ * adds to fpmat to route those callables through this library.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  "dev" buffers are device pointers on
+ *     the context's device, ordered on the context stream; "host" buffers
+ *     are host pointers (pinned or pageable), copied synchronously.
+ *   - Polynomial matrices are dense, entry-major: coefficient t of entry
+ *     (i, j) of an r x c matrix with length L sits at [(i*c + j)*L + t]
+ *     (low degree first, trailing zeros allowed; the reference trims,
+ *     upoly.py:34-37, and compares trimmed lists, polmat.py:184-189).
+ *   - elem_bytes = 4: uint32 elements (requires p < 2^32);
+ *     elem_bytes = 8: uint64 elements (any prime 2 < p < 2^62).
+ *     All inputs must already be reduced into [0, p).
+ *   - Every function returns 0 on success or an FPM_ERR_* code; the message
+ *     is available from fpm_last_error() (thread-local).  Error codes map
+ *     1:1 onto the reference exception classes (fpmat/errors.py).
+ *   - Calls are deterministic: no result depends on atomics ordering.
+ */
+#ifndef FPMAT_B200_H
+#define FPMAT_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exceptions (errors.py) */
+#define FPM_OK 0
+#define FPM_ERR_DIM_MISMATCH 1        /* errors.DimMismatch     (polmat.py:250-253) */
+#define FPM_ERR_CTX_MISMATCH 2        /* errors.CtxMismatch     (polmat.py:241-243) */
+#define FPM_ERR_ORDER_TOO_SMALL 3     /* errors.OrderTooSmall   (polmat.py:295-296) */
+#define FPM_ERR_FIELD_TOO_SMALL 4     /* errors.FieldTooSmall   (polmat.py:397-398) */
+#define FPM_ERR_DEGREE_TOO_LARGE 5    /* errors.DegreeTooLarge  (polmat.py:477-480) */
+#define FPM_ERR_ENVELOPE_EXCEEDED 6   /* errors.EnvelopeExceeded (polmat.py:583-586) */
+#define FPM_ERR_LENGTH_MISMATCH 7     /* errors.LengthMismatch  (modring.py:274-275) */
+#define FPM_ERR_OUT_OF_RANGE 8        /* errors.OutOfRange      (modring.py:157-158) */
+#define FPM_ERR_COMPOSITE_MODULUS 9   /* errors.CompositeModulus (modring.py:159-160) */
+#define FPM_ERR_INVALID_ARGUMENT 20   /* ValueError */
+#define FPM_ERR_UNSUPPORTED 21        /* size outside the implemented kernels */
+#define FPM_ERR_CUDA 30
+#define FPM_ERR_NO_DEVICE 31
+#define FPM_ERR_OUT_OF_MEMORY 32
+
+typedef struct fpm_context fpm_context;
+
+/* ---- runtime ---------------------------------------------------------- */
+int fpm_version(void);
+const char* fpm_last_error(void);
+/* number of kernels this library has launched (all contexts) */
+long long fpm_launch_count(void);
+int fpm_context_create(int device, fpm_context** out);
+void fpm_context_destroy(fpm_context* ctx);
+/* use a caller-owned cudaStream_t (e.g. torch.cuda.current_stream()) */
+int fpm_context_set_stream(fpm_context* ctx, void* cuda_stream);
+int fpm_context_synchronize(fpm_context* ctx);
+
+/* ---- field (modring.field_new, modring.py:151-171) ----------------------
+ * two_adicity and the 2^k-order root (smallest QNR ^ ((p-1) >> k)).
+ * FPM_ERR_OUT_OF_RANGE unless 2 < p < 2^62; FPM_ERR_COMPOSITE_MODULUS. */
+int fpm_field_info(uint64_t p, int* two_adicity, uint64_t* ntt_root);
+
+/* ---- NTT (modring.ntt_forward / ntt_inverse, modring.py:272-286) --------
+ * batch transforms of length 2^log_len, natural order in and out:
+ * forward out[j] = F(w^j) with the reference root w (modring.py:233);
+ * inverse applies w^-1 and scales by N^-1.  dev buffers, batch*N uint32.
+ * Requires p < 2^31, 5 <= log_len <= min(15, two_adicity(p)). */
+int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch,
+                const uint32_t* in_dev, uint32_t* out_dev, int inverse);
+
+/* same contract for any prime 2 < p < 2^62 and any 0 <= log_len <=
+ * two_adicity(p), uint64 elements (direct DFT outside the fast kernel). */
+int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch,
+                const uint64_t* in_dev, uint64_t* out_dev, int inverse);
+
+/* ---- pm_mul (polmat.pm_mul, polmat.py:447-467) ---------------------------
+ * C (m x n, length la+lb-1) = A (m x k, length la) * B (k x n, length lb).
+ * Exact product; identical to every reference strategy.
+ * 31-bit NTT primes run a direct transform; every other prime runs an exact
+ * multi-prime product with CRT reconstruction. */
+int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes,
+                   const void* A_dev, int m, int k, int la,
+                   const void* B_dev, int n, int lb, void* C_dev);
+int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes,
+                        const void* A_host, int m, int k, int la,
+                        const void* B_host, int n, int lb, void* C_host);
+
+/* ---- middle product (polmat._pm_middle / pm_middle_product,
+ *      polmat.py:470-536) ----------------------------------------------------
+ * R (m x n, length d): exact == 0 reproduces the reference `_pm_middle`
+ * bit for bit (including its cyclic fold); exact == 1 returns
+ * the true slice [c, c+d) of A*B (the SPEC S:219 contract).  The checked
+ * public variant raises FPM_ERR_DEGREE_TOO_LARGE like pm_middle_product. */
+int fpm_polmat_middle(fpm_context* ctx, uint64_t p, int elem_bytes,
+                      const void* A_dev, int m, int k, int la,
+                      const void* B_dev, int n, int lb,
+                      long long c, int d, int exact, void* R_dev);
+int fpm_pm_middle_product(fpm_context* ctx, uint64_t p, int elem_bytes,
+                          const void* A_dev, int m, int k, int la,
+                          const void* B_dev, int n, int lb,
+                          long long c, int d, void* R_dev);
+
+/* ---- approximant bases (appint.mbasis / pmbasis, appint.py:143-196) -----
+ * F (m x n, length lf) device; shift: m int64 (host).  P_dev receives the
+ * m x m basis with room for order+1 coefficients; *lp = deg(P)+1.
+ * Output identical to the reference for every base threshold (the result
+ * is the product of the canonical order-1 steps, appint.py:24-60).
+ * rdeg_out (host, optional, m int64): rdeg_s(P) after _finish_shift. */
+int fpm_mbasis(fpm_context* ctx, uint64_t p, int elem_bytes,
+               const void* F_dev, int m, int n, int lf, int order,
+               const int64_t* shift, void* P_dev, int* lp, int64_t* rdeg_out);
+int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes,
+                const void* F_dev, int m, int n, int lf, int order,
+                const int64_t* shift, void* P_dev, int* lp, int64_t* rdeg_out);
+int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes,
+                     const void* F_host, int m, int n, int lf, int order,
+                     const int64_t* shift, void* P_host, int* lp, int64_t* rdeg_out);
+/* base-case threshold used by fpm_pmbasis (default 32, config.py:18) */
+int fpm_set_pmbasis_threshold(fpm_context* ctx, int T);
+
+/* ---- tracing: per-stage device time (CUDA events on the context stream) --
+ * enable (clears previous records), run calls, then read stage i's name and
+ * milliseconds (synchronizes on that stage). */
+int fpm_profile_enable(fpm_context* ctx, int on);
+int fpm_profile_count(fpm_context* ctx);
+int fpm_profile_get(fpm_context* ctx, int i, char* name, int name_len, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPMAT_B200_H */

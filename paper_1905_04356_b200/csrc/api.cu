@@ -1,0 +1,310 @@
+// api.cu -- extern "C" entry points declared in include/fpmat_b200.h.
+#include <cstring>
+#include <new>
+#include <vector>
+#include "../../include/fpmat_b200.h"
+#include "ntt.cuh"
+#include "ops.cuh"
+#include "crt.cuh"
+#include "pmbasis.cuh"
+
+struct fpm_context {
+  fpm::Context* cx;
+  int pmbasis_T;
+};
+
+using namespace fpm;
+
+namespace {
+
+int check_elem(uint64_t p, int elem_bytes) {
+  if (elem_bytes != 4 && elem_bytes != 8) {
+    set_last_error("elem_bytes must be 4 or 8, got %d", elem_bytes);
+    return kInvalidArgument;
+  }
+  if (p <= 2 || p >= (1ull << 62)) {
+    set_last_error("modulus must satisfy 2 < p < 2^62, got %llu", (unsigned long long)p);
+    return kOutOfRange;
+  }
+  if (elem_bytes == 4 && p >= (1ull << 32)) {
+    set_last_error("uint32 elements need p < 2^32");
+    return kInvalidArgument;
+  }
+  return kOk;
+}
+
+int check_dims(int m, int k, int n) {
+  if (m < 0 || k < 0 || n < 0) {
+    set_last_error("negative dimension");
+    return kInvalidArgument;
+  }
+  return kOk;
+}
+
+struct HostStage {
+  Workspace ws;
+  explicit HostStage(Context& cx) : ws(cx) {}
+};
+
+}  // namespace
+
+extern "C" {
+
+int fpm_version(void) { return 100; }
+
+const char* fpm_last_error(void) { return fpm::last_error(); }
+
+long long fpm_launch_count(void) { return fpm::g_launch_count.load(); }
+
+int fpm_context_create(int device, fpm_context** out) {
+  if (!out) return kInvalidArgument;
+  Context* cx = new (std::nothrow) Context(device);
+  if (!cx) return kOutOfMemory;
+  int s = cx->init();
+  if (s != kOk) {
+    delete cx;
+    return s;
+  }
+  *out = new fpm_context{cx, 32};
+  return kOk;
+}
+
+void fpm_context_destroy(fpm_context* ctx) {
+  if (!ctx) return;
+  delete ctx->cx;
+  delete ctx;
+}
+
+int fpm_context_set_stream(fpm_context* ctx, void* stream) {
+  if (!ctx) return kInvalidArgument;
+  return ctx->cx->set_stream((cudaStream_t)stream);
+}
+
+int fpm_context_synchronize(fpm_context* ctx) {
+  if (!ctx) return kInvalidArgument;
+  FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
+  return kOk;
+}
+
+int fpm_field_info(uint64_t p, int* two_adicity, uint64_t* root) {
+  if (p <= 2 || p >= (1ull << 62)) {
+    set_last_error("modulus must satisfy 2 < p < 2^62, got %llu", (unsigned long long)p);
+    return kOutOfRange;
+  }
+  if (!h_is_prime(p)) {
+    set_last_error("%llu is not prime", (unsigned long long)p);
+    return kCompositeModulus;
+  }
+  if (two_adicity) *two_adicity = h_two_adicity(p);
+  if (root) *root = h_ntt_root(p);
+  return kOk;
+}
+
+int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch, const uint32_t* in,
+                uint32_t* out, int inverse) {
+  if (!ctx) return kInvalidArgument;
+  if (p >= (1u << 31) || p <= 2) {
+    set_last_error("fpm_ntt_u32 needs 2 < p < 2^31");
+    return kOutOfRange;
+  }
+  if (log_len > h_two_adicity(p)) {
+    set_last_error("p=%u supports transforms up to length 2^%d", p, h_two_adicity(p));
+    return kOutOfRange;
+  }
+  if (log_len < kMinLogN || log_len > kMaxLogN) {
+    set_last_error("fpm_ntt_u32 supports 2^%d..2^%d", kMinLogN, kMaxLogN);
+    return kUnsupported;
+  }
+  Context& cx = *ctx->cx;
+  PrimeSet ps;
+  ps.count = 1;
+  FPM_TRY(cx.prime_const(p, log_len, &ps.pr[0]));
+  if (!inverse) {
+    NttFwdArgs a{};
+    a.in = in; a.in64 = 0; a.in_stride = 1LL << log_len; a.len = 1 << log_len;
+    a.reduce = 0; a.fold = 0; a.natural = 1; a.n_entries = batch; a.out = out;
+    return launch_ntt_fwd(log_len, a, ps, cx.stream());
+  }
+  NttInvArgs a{};
+  a.in = in; a.natural = 1; a.n_entries = batch; a.out = out;
+  a.out_stride = 1LL << log_len; a.out_len = 1 << log_len; a.off = 0; a.scale = 1;
+  return launch_ntt_inv(log_len, a, ps, cx.stream());
+}
+
+int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch, const uint64_t* in,
+                uint64_t* out, int inverse) {
+  if (!ctx) return kInvalidArgument;
+  if (p <= 2 || p >= (1ull << 62)) {
+    set_last_error("modulus must satisfy 2 < p < 2^62");
+    return kOutOfRange;
+  }
+  const int k = h_two_adicity(p);
+  if (log_len < 0 || log_len > k) {
+    set_last_error("p=%llu supports transforms up to length 2^%d", (unsigned long long)p, k);
+    return kOutOfRange;
+  }
+  if (log_len > 20) {
+    set_last_error("direct DFT limited to 2^20 points");
+    return kUnsupported;
+  }
+  const uint64_t N = 1ull << log_len;
+  uint64_t omega = h_powmod(h_ntt_root(p), 1ull << (k - log_len), p);
+  uint64_t scale = 1;
+  if (inverse) {
+    omega = h_invmod(omega, p);
+    scale = h_invmod(N % p, p);
+  }
+  return launch_dft_direct(p, omega, (int)N, batch, in, out, scale, ctx->cx->stream());
+}
+
+int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m, int k,
+                   int la, const void* B, int n, int lb, void* C) {
+  if (!ctx) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  FPM_TRY(check_dims(m, k, n));
+  const int is64 = elem_bytes == 8;
+  const int lc = (la > 0 && lb > 0) ? la + lb - 1 : 0;
+  MatRef Ar{A, is64, la, la};
+  MatRef Br{B, is64, lb, lb};
+  OutRef Cr{C, is64, lc, lc};
+  return polmat_mul(*ctx->cx, p, m, k, n, Ar, Br, Cr);
+}
+
+int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
+                        int k, int la, const void* B, int n, int lb, void* C) {
+  if (!ctx) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  FPM_TRY(check_dims(m, k, n));
+  Context& cx = *ctx->cx;
+  Workspace ws(cx);
+  const size_t esz = elem_bytes;
+  const size_t na = (size_t)m * k * (la > 0 ? la : 0), nb = (size_t)k * n * (lb > 0 ? lb : 0);
+  const int lc = (la > 0 && lb > 0) ? la + lb - 1 : 0;
+  const size_t nc = (size_t)m * n * lc;
+  unsigned char *dA, *dB, *dC;
+  FPM_TRY(ws.get(esz * na + 1, &dA));
+  FPM_TRY(ws.get(esz * nb + 1, &dB));
+  FPM_TRY(ws.get(esz * nc + 1, &dC));
+  if (na) FPM_CUDA_TRY(cudaMemcpyAsync(dA, A, esz * na, cudaMemcpyHostToDevice, cx.stream()));
+  if (nb) FPM_CUDA_TRY(cudaMemcpyAsync(dB, B, esz * nb, cudaMemcpyHostToDevice, cx.stream()));
+  FPM_TRY(fpm_polmat_mul(ctx, p, elem_bytes, dA, m, k, la, dB, n, lb, dC));
+  if (nc) FPM_CUDA_TRY(cudaMemcpyAsync(C, dC, esz * nc, cudaMemcpyDeviceToHost, cx.stream()));
+  FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
+  return kOk;
+}
+
+int fpm_polmat_middle(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
+                      int k, int la, const void* B, int n, int lb, long long c, int d, int exact,
+                      void* R) {
+  if (!ctx) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  FPM_TRY(check_dims(m, k, n));
+  if (d <= 0) return kOk;
+  if (c < 0) {
+    set_last_error("middle product offset c must be >= 0");
+    return kInvalidArgument;
+  }
+  Context& cx = *ctx->cx;
+  const int is64 = elem_bytes == 8;
+  int da = -1, db = -1;
+  FPM_TRY(matrix_degree(cx, A, is64, (long long)m * k, la, &da));
+  FPM_TRY(matrix_degree(cx, B, is64, (long long)k * n, lb, &db));
+  MatRef Ar{A, is64, la, la};
+  MatRef Br{B, is64, lb, lb};
+  OutRef Rr{R, is64, d, d};
+  return polmat_middle(cx, p, m, k, n, Ar, Br, da, db, c, d, exact, Rr);
+}
+
+int fpm_pm_middle_product(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
+                          int k, int la, const void* B, int n, int lb, long long c, int d,
+                          void* R) {
+  // polmat.pm_middle_product contract (polmat.py:476-481)
+  if (!ctx) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  Context& cx = *ctx->cx;
+  const int is64 = elem_bytes == 8;
+  int da = -1, db = -1;
+  FPM_TRY(matrix_degree(cx, A, is64, (long long)m * k, la, &da));
+  FPM_TRY(matrix_degree(cx, B, is64, (long long)k * n, lb, &db));
+  if (da >= c && c > 0) {
+    set_last_error("deg A = %d must be < c = %lld", da, c);
+    return kDegreeTooLarge;
+  }
+  if (db >= c + d) {
+    set_last_error("deg B = %d must be < c+d = %lld", db, c + d);
+    return kDegreeTooLarge;
+  }
+  return fpm_polmat_middle(ctx, p, elem_bytes, A, m, k, la, B, n, lb, c, d, 0, R);
+}
+
+int fpm_mbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n, int lf,
+               int order, const int64_t* shift, void* P, int* lp, int64_t* rdeg_out) {
+  if (!ctx || !lp || (m > 0 && !shift)) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (m <= 0 || n < 0 || order < 0) {
+    set_last_error("mbasis needs m >= 1, n >= 0, order >= 0");
+    return kInvalidArgument;
+  }
+  return mbasis_run(*ctx->cx, p, elem_bytes == 8, F, m, n, lf, lf, order, shift, P, order + 1,
+                    lp, rdeg_out);
+}
+
+int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n,
+                int lf, int order, const int64_t* shift, void* P, int* lp, int64_t* rdeg_out) {
+  if (!ctx || !lp || (m > 0 && !shift)) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (m <= 0 || n < 0 || order < 0) {
+    set_last_error("pmbasis needs m >= 1, n >= 0, order >= 0");
+    return kInvalidArgument;
+  }
+  return pmbasis_run(*ctx->cx, p, elem_bytes == 8, F, m, n, lf, lf, order, shift,
+                     ctx->pmbasis_T, P, order + 1, lp, rdeg_out);
+}
+
+int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n,
+                     int lf, int order, const int64_t* shift, void* P, int* lp,
+                     int64_t* rdeg_out) {
+  if (!ctx || !lp) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (m <= 0 || n < 0 || order < 0 || lf < 0) {
+    set_last_error("pmbasis needs m >= 1, n >= 0, order >= 0");
+    return kInvalidArgument;
+  }
+  Context& cx = *ctx->cx;
+  Workspace ws(cx);
+  const size_t esz = elem_bytes;
+  const size_t nf = (size_t)m * n * lf, np = (size_t)m * m * (order + 1);
+  unsigned char *dF, *dP;
+  FPM_TRY(ws.get(esz * nf + 1, &dF));
+  FPM_TRY(ws.get(esz * np + 1, &dP));
+  if (nf) FPM_CUDA_TRY(cudaMemcpyAsync(dF, F, esz * nf, cudaMemcpyHostToDevice, cx.stream()));
+  FPM_TRY(fpm_pmbasis(ctx, p, elem_bytes, dF, m, n, lf, order, shift, dP, lp, rdeg_out));
+  FPM_CUDA_TRY(cudaMemcpyAsync(P, dP, esz * np, cudaMemcpyDeviceToHost, cx.stream()));
+  FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
+  return kOk;
+}
+
+int fpm_profile_enable(fpm_context* ctx, int on) {
+  if (!ctx) return kInvalidArgument;
+  ctx->cx->profile_enable(on != 0);
+  return kOk;
+}
+
+int fpm_profile_count(fpm_context* ctx) { return ctx ? ctx->cx->profile_count() : 0; }
+
+int fpm_profile_get(fpm_context* ctx, int i, char* name, int name_len, float* ms) {
+  if (!ctx || !name || name_len <= 0 || !ms) return kInvalidArgument;
+  const char* nm = nullptr;
+  FPM_TRY(ctx->cx->profile_get(i, &nm, ms));
+  std::strncpy(name, nm ? nm : "", (size_t)name_len - 1);
+  name[name_len - 1] = 0;
+  return kOk;
+}
+
+int fpm_set_pmbasis_threshold(fpm_context* ctx, int T) {
+  if (!ctx || T < 1) return kInvalidArgument;
+  ctx->pmbasis_T = T;
+  return kOk;
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// common.cuh -- shared types, modular arithmetic and error plumbing for the
+// B200 F_p polynomial-matrix library (libfpm_b200.so).
+//
+// Word-size arithmetic conventions (all kernels):
+//   * NTT primes are < 2^31, so 2p < 2^32 and every value lives in [0, p)
+//     between butterflies; DIF butterflies feed the unreduced difference
+//     (< 2p) straight into a Shoup multiply (Harvey's trick restricted to the
+//     one place 2^32 > 2p allows it).
+//   * Twiddles are stored as (w, w') with w' = floor(w * 2^32 / p) (Shoup).
+//   * Pointwise accumulation is 64-bit with a periodic fold
+//     acc = hi(acc) * (2^32 mod p) + lo(acc); see pointwise.cu.
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+#include <atomic>
+
+namespace fpm {
+
+// ---- status codes (mirror include/fpmat_b200.h) ---------------------------
+enum Status : int {
+  kOk = 0,
+  kDimMismatch = 1,
+  kCtxMismatch = 2,
+  kOrderTooSmall = 3,
+  kFieldTooSmall = 4,
+  kDegreeTooLarge = 5,
+  kEnvelopeExceeded = 6,
+  kLengthMismatch = 7,
+  kOutOfRange = 8,
+  kCompositeModulus = 9,
+  kInvalidArgument = 20,
+  kUnsupported = 21,
+  kCudaError = 30,
+  kNoDevice = 31,
+  kOutOfMemory = 32,
+};
+
+extern std::atomic<long long> g_launch_count;  // kernels launched (all contexts)
+void set_last_error(const char* fmt, ...);
+const char* last_error();
+
+#define FPM_CUDA_TRY(expr)                                                     \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::fpm::set_last_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,      \
+                            cudaGetErrorString(_e));                           \
+      return ::fpm::kCudaError;                                                \
+    }                                                                          \
+  } while (0)
+
+#define FPM_TRY(expr)                                                          \
+  do {                                                                         \
+    int _s = (expr);                                                           \
+    if (_s != ::fpm::kOk) return _s;                                           \
+  } while (0)
+
+#define FPM_LAUNCH_CHECK()                                                     \
+  do {                                                                         \
+    ::fpm::g_launch_count.fetch_add(1, std::memory_order_relaxed);             \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::fpm::set_last_error("%s:%d: kernel launch -> %s", __FILE__, __LINE__,  \
+                            cudaGetErrorString(_e));                           \
+      return ::fpm::kCudaError;                                                \
+    }                                                                          \
+  } while (0)
+
+// ---- host-side exact arithmetic ---------------------------------------------
+typedef unsigned __int128 u128;
+
+static inline uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t p) {
+  return (uint64_t)((u128)a * b % p);
+}
+static inline uint64_t h_powmod(uint64_t a, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p;
+  a %= p;
+  while (e) {
+    if (e & 1) r = h_mulmod(r, a, p);
+    a = h_mulmod(a, a, p);
+    e >>= 1;
+  }
+  return r;
+}
+static inline uint64_t h_invmod(uint64_t a, uint64_t p) { return h_powmod(a, p - 2, p); }
+static inline uint32_t h_shoup(uint32_t w, uint32_t p) {
+  return (uint32_t)(((uint64_t)w << 32) / p);
+}
+bool h_is_prime(uint64_t n);          // deterministic Miller-Rabin (modring.py:25-47)
+int h_two_adicity(uint64_t p);        // modring.py:161-165
+uint64_t h_ntt_root(uint64_t p);      // smallest QNR ^ ((p-1) >> k), modring.py:166-170
+
+// ---- device helpers ---------------------------------------------------------
+__device__ __forceinline__ uint32_t d_red(uint32_t x, uint32_t p) {
+  // x in [0, 2p) -> [0, p); unsigned min trick (x - p wraps when x < p)
+  return min(x, x - p);
+}
+// Shoup multiply: any a < 2^32, w < p, wp = floor(w 2^32 / p) -> [0, 2p)
+__device__ __forceinline__ uint32_t d_shoup(uint32_t a, uint32_t w, uint32_t wp,
+                                            uint32_t p) {
+  uint32_t q = __umulhi(a, wp);
+  return a * w - q * p;
+}
+// full reduction of a 64-bit value: x mod p for p < 2^31
+// mu = floor(2^64 / p) (needs p not a power of two; p odd prime > 2)
+__device__ __forceinline__ uint32_t d_red64(uint64_t x, uint32_t p, uint64_t mu) {
+  uint64_t q = __umul64hi(x, mu);
+  uint64_t r = x - q * (uint64_t)p;  // < 2p (Barrett error <= 1)
+  uint32_t r32 = (uint32_t)r;
+  return r >= p ? r32 - p : r32;
+}
+
+// Per-prime constants handed to kernels by value.
+struct PrimeConst {
+  uint32_t p;
+  uint32_t c32;      // 2^32 mod p (pointwise fold)
+  uint64_t mu;       // floor(2^64 / p) (Barrett)
+  uint32_t ninv;     // N^-1 mod p for the transform length in use
+  uint32_t ninv_sh;  // Shoup companion of ninv
+  const uint2* tw;   // forward (w, w') table, N/2 entries
+  const uint2* itw;  // inverse table, N/2 entries
+};
+
+constexpr int kMaxPrimes = 8;
+struct PrimeSet {
+  int count;
+  PrimeConst pr[kMaxPrimes];
+};
+
+}  // namespace fpm

@@ -1,0 +1,266 @@
+// crt.cu -- Garner CRT, generic-modulus middle product, degree helpers.
+#include "crt.cuh"
+#include <climits>
+
+namespace fpm {
+
+__device__ __forceinline__ uint64_t d_montmul(uint64_t a, uint64_t b, uint64_t P, uint64_t Pni) {
+  // (a*b + m*P) / 2^64 with m = -a*b*P^-1 mod 2^64; a*b < 2^64 * P required
+  const uint64_t lo = a * b, hi = __umul64hi(a, b);
+  const uint64_t m = lo * Pni;
+  const uint64_t mh = __umul64hi(m, P);
+  uint64_t r = hi + mh + (lo != 0);
+  r = r >= P ? r - P : r;
+  return r >= P ? r - P : r;
+}
+__device__ __forceinline__ uint64_t d_mulmod_any(uint64_t a, uint64_t b, uint64_t P,
+                                                 uint64_t Pni, uint64_t R2) {
+  return d_montmul(d_montmul(a, R2, P, Pni), b, P, Pni);
+}
+__device__ __forceinline__ uint64_t d_addmod64(uint64_t a, uint64_t b, uint64_t P) {
+  const uint64_t s = a + b;  // P < 2^62
+  return s >= P ? s - P : s;
+}
+
+namespace {
+
+__global__ void crt_kernel(CrtArgs a) {
+  const long long total = (long long)a.n_entries * a.len;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long e = idx / a.len;
+    const int t = (int)(idx - e * a.len);
+    const uint32_t* src = a.res + e * a.res_stride + t;
+    uint32_t v[kMaxPrimes];
+#pragma unroll
+    for (int i = 0; i < kMaxPrimes; ++i) {
+      if (i >= a.r) break;
+      const uint32_t qi = a.q[i];
+      uint32_t x = src[i * a.res_prime_stride];
+#pragma unroll
+      for (int j = 0; j < kMaxPrimes; ++j) {
+        if (j >= i) break;
+        const uint32_t vj = v[j] >= qi ? v[j] - qi : v[j];
+        x = x - vj + qi;  // [1, 2 qi)
+        x = d_red(d_shoup(x, a.g[j][i], a.gsh[j][i], qi), qi);
+      }
+      v[i] = x;
+    }
+    uint64_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxPrimes; ++i) {
+      if (i >= a.r) break;
+      s = d_addmod64(s, d_montmul(v[i], a.Mmont[i], a.P, a.Pni), a.P);
+    }
+    if (a.out64)
+      ((uint64_t*)a.out)[e * a.out_stride + t] = s;
+    else
+      ((uint32_t*)a.out)[e * a.out_stride + t] = (uint32_t)s;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ int trimmed_len(const T* e, int L) {
+  while (L > 0 && e[L - 1] == 0) --L;
+  return L;
+}
+
+template <typename Tin, typename Tout>
+__global__ void middle_entrywise_kernel(MiddleEntryArgs a) {
+  const Tin* A = (const Tin*)a.A;
+  const Tin* B = (const Tin*)a.B;
+  Tout* out = (Tout*)a.out;
+  const long long total = (long long)a.m * a.n * a.d;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long ij = idx / a.d;
+    const int tt = (int)(idx - ij * a.d);
+    const int i = (int)(ij / a.n), j = (int)(ij - (long long)i * a.n);
+    const long long t = a.c + tt;
+    uint64_t acc = 0;
+    for (int l = 0; l < a.k; ++l) {
+      const Tin* ae = A + ((long long)i * a.k + l) * a.la;
+      const Tin* be = B + ((long long)l * a.n + j) * a.lb;
+      const int la = trimmed_len(ae, a.la), lb = trimmed_len(be, a.lb);
+      if (la == 0 || lb == 0) continue;
+      const long long lad = (long long)la * a.d;
+      bool cyclic = false;
+      long long Ne = 0;
+      if (!(lad <= 64 * 64 / 4 && lad <= 16384)) {
+        const long long need = (long long)la + a.d;
+        int lg = 0;
+        while ((1LL << lg) < need) ++lg;  // max(1, (need-1).bit_length())
+        if (lg < 1) lg = 1;
+        if (lg <= a.two_adicity) { cyclic = true; Ne = 1LL << lg; }
+      }
+      if (!cyclic) {
+        // exact coefficient t of a*b (schoolbook or full-product slice)
+        long long lo = t - lb + 1 > 0 ? t - lb + 1 : 0;
+        long long hi = la - 1 < t ? la - 1 : t;
+        for (long long u = lo; u <= hi; ++u)
+          acc = d_addmod64(acc, d_mulmod_any((uint64_t)ae[u], (uint64_t)be[t - u], a.P, a.Pni, a.R2), a.P);
+      } else {
+        // cyclic fold mod x^Ne - 1 (upoly.py:366-374): sum a_u b_w, u+w = t mod Ne
+        const long long tm = t % Ne;
+        for (int u = 0; u < la; ++u) {
+          long long w0 = tm - u;
+          w0 %= Ne;
+          if (w0 < 0) w0 += Ne;
+          for (long long w = w0; w < lb; w += Ne)
+            acc = d_addmod64(acc, d_mulmod_any((uint64_t)ae[u], (uint64_t)be[w], a.P, a.Pni, a.R2), a.P);
+        }
+      }
+    }
+    out[ij * a.d + tt] = (Tout)acc;
+  }
+}
+
+template <typename T>
+__global__ void max_len_kernel(const T* M, long long entries, int L, int* out) {
+  int best = 0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < entries;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int l = trimmed_len(M + e * L, L);
+    best = l > best ? l : best;
+  }
+  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best > 0) atomicMax(out, best);
+}
+
+template <typename T>
+__global__ void rdeg_kernel(const T* M, int rows, int cols, int L, const int64_t* s, int64_t* out) {
+  // one warp per row
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  long long best = LLONG_MIN, smin = LLONG_MAX;
+  for (int j = lane; j < cols; j += 32) {
+    smin = min(smin, (long long)s[j]);
+    const int l = trimmed_len(M + ((long long)row * cols + j) * L, L);
+    if (l > 0) best = max(best, (long long)(l - 1) + (long long)s[j]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
+    smin = min(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+  }
+  if (lane == 0) out[row] = best == LLONG_MIN ? smin : best;
+}
+
+__global__ void dft_direct_kernel(uint64_t P, uint64_t Pni, uint64_t R2, uint64_t omega, int N,
+                                  int batch, const uint64_t* in, uint64_t* out, uint64_t scale) {
+  const long long total = (long long)batch * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long b = idx / N;
+    const int j = (int)(idx - b * N);
+    // w^j by square-and-multiply, then Horner-free accumulation sum in[t] (w^j)^t
+    uint64_t wj = 1, base = omega;
+    for (int e = j; e; e >>= 1) {
+      if (e & 1) wj = d_mulmod_any(wj, base, P, Pni, R2);
+      base = d_mulmod_any(base, base, P, Pni, R2);
+    }
+    const uint64_t* v = in + b * N;
+    uint64_t acc = 0, pw = 1;
+    for (int t = 0; t < N; ++t) {
+      acc = d_addmod64(acc, d_mulmod_any(v[t], pw, P, Pni, R2), P);
+      pw = d_mulmod_any(pw, wj, P, Pni, R2);
+    }
+    out[idx] = d_mulmod_any(acc, scale, P, Pni, R2);
+  }
+}
+
+}  // namespace
+
+int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64_t* in,
+                      uint64_t* out, uint64_t scale, cudaStream_t st) {
+  const long long total = (long long)batch * N;
+  if (total <= 0) return kOk;
+  CrtArgs tmp{};
+  const uint32_t q1 = 2013265921u;
+  crt_prepare(tmp, &q1, 1, p);
+  const u128 R = ((u128)1 << 64) % p;
+  const uint64_t R2 = (uint64_t)(R * R % p);
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  dft_direct_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, tmp.Pni, R2, omega, N, batch, in, out,
+                                                      scale);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+void crt_prepare(CrtArgs& a, const uint32_t* q, int r, uint64_t P) {
+  a.r = r;
+  for (int i = 0; i < r; ++i) a.q[i] = q[i];
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < i; ++j) {
+      const uint32_t inv = (uint32_t)h_invmod(q[j] % q[i], q[i]);
+      a.g[j][i] = inv;
+      a.gsh[j][i] = h_shoup(inv, q[i]);
+    }
+  a.P = P;
+  // -P^-1 mod 2^64 by Newton iteration
+  uint64_t inv = P;  // correct to 3 bits for odd P
+  for (int it = 0; it < 6; ++it) inv *= 2 - P * inv;
+  a.Pni = (uint64_t)0 - inv;
+  uint64_t prod = 1 % P;
+  const u128 R = ((u128)1 << 64) % P;
+  for (int i = 0; i < r; ++i) {
+    a.Mmont[i] = (uint64_t)((u128)prod * R % P);
+    prod = h_mulmod(prod, q[i] % P, P);
+  }
+}
+
+int launch_crt(const CrtArgs& a, cudaStream_t st) {
+  const long long total = (long long)a.n_entries * a.len;
+  if (total <= 0) return kOk;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  crt_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_middle_entrywise(const MiddleEntryArgs& a, cudaStream_t st) {
+  const long long total = (long long)a.m * a.n * a.d;
+  if (total <= 0) return kOk;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (a.in64 && a.out64)
+    middle_entrywise_kernel<uint64_t, uint64_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else if (!a.in64 && !a.out64)
+    middle_entrywise_kernel<uint32_t, uint32_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+  else {
+    set_last_error("middle_entrywise: mixed element widths unsupported");
+    return kInvalidArgument;
+  }
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_max_len(const void* M, int in64, long long entries, int L, int* out, cudaStream_t st) {
+  FPM_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int), st));
+  if (entries <= 0 || L <= 0) return kOk;
+  long long blocks = (entries + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (in64)
+    max_len_kernel<uint64_t><<<(unsigned)blocks, 256, 0, st>>>((const uint64_t*)M, entries, L, out);
+  else
+    max_len_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>((const uint32_t*)M, entries, L, out);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_rdeg(const void* M, int in64, int rows, int cols, int L, const int64_t* s,
+                int64_t* out, cudaStream_t st) {
+  if (rows <= 0) return kOk;
+  const int wpb = 8;
+  const unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
+  if (in64)
+    rdeg_kernel<uint64_t><<<blocks, wpb * 32, 0, st>>>((const uint64_t*)M, rows, cols, L, s, out);
+  else
+    rdeg_kernel<uint32_t><<<blocks, wpb * 32, 0, st>>>((const uint32_t*)M, rows, cols, L, s, out);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+}  // namespace fpm

@@ -1,0 +1,62 @@
+// ntt.cuh -- batched forward/inverse NTT over 31-bit primes (sm_100a).
+//
+// Replaces modring.ntt_forward / ntt_inverse (modring.py:253-286) and the
+// per-entry evaluation / interpolation loops of polmat._pm_mul_ntt
+// (polmat.py:275-307) and polmat._pm_middle (polmat.py:498-521).
+//
+// Design (DESIGN.md section "NTT"):
+//  * one transform of N = 2^LOGN (32 <= N <= 32768) is held by N/32 threads,
+//    32 values each in registers; the LOGN DIF stages are split in passes of
+//    <= 5 bits (radix-32 register butterflies), passes exchange through a
+//    padded shared-memory tile (index x + x/32 => bank-conflict free);
+//  * forward = Gentleman-Sande DIF (natural -> bit-reversed order), inverse =
+//    Cooley-Tukey DIT (bit-reversed -> natural), so the product path never
+//    permutes: evaluation points stay in DIF order between the transforms and
+//    the pointwise stage, which is order agnostic;
+//  * evaluations are written in the blocked point-major "eval layout"
+//        E[t / 32][entry][t % 32]
+//    so each thread stores one full 128-byte line per entry and the pointwise
+//    kernel reads all entries of a 32-point block contiguously;
+//  * twiddles come from a per-(p, N) table of (w, floor(w 2^32 / p)) pairs;
+//    per-thread table offsets are hoisted so the inner loop is one LDG.64
+//    with an immediate offset per butterfly (L1 resident, shared by all CTAs).
+#pragma once
+#include "common.cuh"
+
+namespace fpm {
+
+struct NttFwdArgs {
+  const void* in;            // coefficients, entry e at in + e * in_stride
+  long long in_stride;       // elements between consecutive entries
+  long long in_prime_stride; // elements between per-prime input copies (0 = shared)
+  int in64;                  // 1: uint64 elements, 0: uint32
+  int len;                   // coefficients to read per entry (zero-padded to N)
+  int fold;                  // len > N: fold cyclically mod x^N - 1
+  int reduce;                // inputs may be >= p: reduce on load
+  int natural;               // 1: natural-order output out[e*N + k] (public API)
+  int n_entries;
+  uint32_t* out;             // eval layout E[N/32][n_entries][32] (or natural)
+  long long out_prime_stride;
+};
+
+struct NttInvArgs {
+  const uint32_t* in;        // eval layout (or natural when natural != 0)
+  long long in_prime_stride;
+  int natural;               // 1: natural-order input in[e*N + k] (public API)
+  int n_entries;
+  uint32_t* out;             // out[e * out_stride + t] = coeff[(off + t) mod N]
+  long long out_stride;
+  long long out_prime_stride;
+  int out_len;
+  int off;
+  int scale;                 // multiply by N^-1 (1 for the product path)
+};
+
+// host launchers (ntt.cu); LOGN in [5, 15]
+int launch_ntt_fwd(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
+int launch_ntt_inv(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
+
+constexpr int kMinLogN = 5;
+constexpr int kMaxLogN = 15;
+
+}  // namespace fpm

@@ -1,0 +1,278 @@
+// ops.cu -- evaluation/interpolation product engine (direct and multi-prime).
+#include "ops.cuh"
+#include <cmath>
+#include "crt.cuh"
+#include "ntt.cuh"
+#include "pointwise.cuh"
+
+namespace fpm {
+
+// NTT primes for the multi-prime path: 31-bit, two-adicity >= 24, largest first
+static const uint32_t kCrtPrimes[] = {2130706433u, 2113929217u, 2013265921u, 1811939329u,
+                                      1711276033u, 1224736769u, 1107296257u};
+static const int kNumCrtPrimes = 7;
+
+int ceil_log2_min1(long long need) {
+  int b = 0;
+  long long x = need - 1;
+  while (x > 0) { ++b; x >>= 1; }
+  return b < 1 ? 1 : b;
+}
+
+namespace {
+
+__global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* out,
+                             long long out_stride, long long entries, int len) {
+  const long long total = entries * len;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i / len;
+    const int t = (int)(i - e * len);
+    out[e * out_stride + t] = in[e * in_stride + t];
+  }
+}
+
+__global__ void zero_tail_kernel(void* out, int is64, long long stride, long long entries,
+                                 int from, int to) {
+  const int w = to - from;
+  const long long total = entries * w;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i / w;
+    const int t = from + (int)(i - e * w);
+    if (is64)
+      ((uint64_t*)out)[e * stride + t] = 0;
+    else
+      ((uint32_t*)out)[e * stride + t] = 0;
+  }
+}
+
+unsigned grid_for(long long total) {
+  long long b = (total + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+int zero_out(OutRef C, long long entries, int from, int to, cudaStream_t st) {
+  if (to <= from || entries <= 0) return kOk;
+  zero_tail_kernel<<<grid_for(entries * (to - from)), 256, 0, st>>>(C.ptr, C.is64, C.stride,
+                                                                   entries, from, to);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+bool direct_ok(uint64_t p, int logn) {
+  return p < (1ull << 31) && p > 2 && h_two_adicity(p) >= logn;
+}
+
+}  // namespace
+
+int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L, int* deg) {
+  if (entries <= 0 || L <= 0) {
+    *deg = -1;
+    return kOk;
+  }
+  Workspace ws(cx);
+  int* d = nullptr;
+  FPM_TRY(ws.get(1, &d));
+  FPM_TRY(launch_max_len(M, is64, entries, L, d, cx.stream()));
+  int h = 0;
+  FPM_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, cx.stream()));
+  FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
+  *deg = h - 1;
+  return kOk;
+}
+
+int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                   int logn, long long off, OutRef C) {
+  cudaStream_t st = cx.stream();
+  const long long ec = (long long)m * n;
+  if (ec == 0 || C.len <= 0) return kOk;
+  if (k == 0 || A.len <= 0 || B.len <= 0) return zero_out(C, ec, 0, C.len, st);
+  if (logn < kMinLogN) logn = kMinLogN;  // a larger cyclic length is exact as well
+  if (logn > kMaxLogN) {
+    set_last_error("transform length 2^%d exceeds the single-CTA NTT limit 2^%d", logn,
+                   kMaxLogN);
+    return kUnsupported;
+  }
+  const long long N = 1LL << logn;
+  const int fold = B.len > N ? 1 : 0;
+  if (A.len > N) {
+    set_last_error("left operand longer than the cyclic length");
+    return kInvalidArgument;
+  }
+  const int wlen = C.len < N ? C.len : (int)N;  // coefficients carrying data
+  off %= N;
+
+  // ---- prime selection -----------------------------------------------------
+  uint32_t primes[kMaxPrimes];
+  int r = 0;
+  bool direct = direct_ok(p, logn);
+  if (direct) {
+    primes[r++] = (uint32_t)p;
+  } else {
+    // exact integer cyclic convolution needs prod(q) > bound
+    const double nfold = fold ? std::ceil((double)B.len / (double)N) : 1.0;
+    double terms = (double)A.len;
+    if (!fold && B.len < terms) terms = (double)B.len;
+    if (terms > (double)N) terms = (double)N;
+    const double lg = std::log2((double)k) + std::log2(terms) + std::log2(nfold) +
+                      2.0 * std::log2((double)(p - 1)) + 2.0;
+    double have = 0.0;
+    for (int i = 0; i < kNumCrtPrimes && have <= lg; ++i) {
+      if (h_two_adicity(kCrtPrimes[i]) < logn) continue;
+      primes[r++] = kCrtPrimes[i];
+      have += std::log2((double)kCrtPrimes[i]);
+    }
+    if (have <= lg) {
+      set_last_error("coefficient bound 2^%.1f exceeds the multi-prime capacity", lg);
+      return kUnsupported;
+    }
+  }
+  PrimeSet ps;
+  ps.count = r;
+  for (int i = 0; i < r; ++i) FPM_TRY(cx.prime_const(primes[i], logn, &ps.pr[i]));
+
+  // ---- workspaces ------------------------------------------------------------
+  Workspace ws(cx);
+  const long long ea = (long long)m * k, eb = (long long)k * n;
+  uint32_t *EA, *EB, *EC;
+  FPM_TRY(ws.get(r * N * ea, &EA));
+  FPM_TRY(ws.get(r * N * eb, &EB));
+  FPM_TRY(ws.get(r * N * ec, &EC));
+
+  const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
+  // forward transforms (all primes in one launch: blockIdx.z = prime)
+  NttFwdArgs fa{};
+  fa.in = A.ptr; fa.in64 = A.is64; fa.in_stride = A.stride; fa.in_prime_stride = 0;
+  fa.len = A.len; fa.fold = 0; fa.reduce = reduce_needed || (!direct && A.is64);
+  fa.natural = 0; fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
+  if (direct && A.is64) fa.reduce = 0;
+  {
+    StageTimer t_(cx, "ntt_fwd_A");
+    FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
+  }
+  NttFwdArgs fb = fa;
+  fb.in = B.ptr; fb.in64 = B.is64; fb.in_stride = B.stride; fb.len = B.len; fb.fold = fold;
+  fb.reduce = reduce_needed || (!direct && B.is64);
+  if (direct && B.is64) fb.reduce = 0;
+  fb.n_entries = (int)eb; fb.out = EB; fb.out_prime_stride = N * eb;
+  {
+    StageTimer t_(cx, "ntt_fwd_B");
+    FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
+  }
+
+  PointwiseArgs pa{};
+  pa.A = EA; pa.B = EB; pa.C = EC; pa.m = m; pa.k = k; pa.n = n; pa.nblk = (int)(N / 32);
+  pa.a_prime_stride = N * ea; pa.b_prime_stride = N * eb; pa.c_prime_stride = N * ec;
+  {
+    StageTimer t_(cx, "pointwise");
+    FPM_TRY(launch_pointwise(pa, ps, st));
+  }
+
+  NttInvArgs ia{};
+  ia.in = EC; ia.in_prime_stride = N * ec; ia.natural = 0; ia.n_entries = (int)ec;
+  ia.out_len = wlen; ia.off = (int)off; ia.scale = 1;
+  if (direct && !C.is64) {
+    ia.out = (uint32_t*)C.ptr; ia.out_stride = C.stride; ia.out_prime_stride = 0;
+    StageTimer t_(cx, "ntt_inv");
+    FPM_TRY(launch_ntt_inv(logn, ia, ps, st));
+  } else {
+    uint32_t* R;
+    FPM_TRY(ws.get((long long)r * ec * wlen, &R));
+    ia.out = R; ia.out_stride = wlen; ia.out_prime_stride = ec * wlen;
+    {
+      StageTimer t_(cx, "ntt_inv");
+      FPM_TRY(launch_ntt_inv(logn, ia, ps, st));
+    }
+    StageTimer t2_(cx, direct ? "widen" : "crt");
+    if (direct) {
+      widen_kernel<<<grid_for(ec * wlen), 256, 0, st>>>(R, wlen, (uint64_t*)C.ptr, C.stride,
+                                                      ec, wlen);
+      FPM_LAUNCH_CHECK();
+    } else {
+      CrtArgs ca{};
+      crt_prepare(ca, primes, r, p);
+      ca.res = R; ca.res_prime_stride = ec * wlen; ca.res_stride = wlen;
+      ca.n_entries = (int)ec; ca.len = wlen;
+      ca.out = C.ptr; ca.out64 = C.is64; ca.out_stride = C.stride;
+      FPM_TRY(launch_crt(ca, st));
+    }
+  }
+  return zero_out(C, ec, wlen, C.len, st);
+}
+
+int polmat_mul(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B, OutRef C) {
+  if (A.len <= 0 || B.len <= 0 || k == 0)
+    return zero_out(C, (long long)m * n, 0, C.len, cx.stream());
+  const long long need = (long long)A.len + B.len - 1;
+  const int logn = ceil_log2_min1(need);
+  return cyclic_product(cx, p, m, k, n, A, B, logn, 0, C);
+}
+
+int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                  int da, int db, long long c, int d, int exact, OutRef C) {
+  cudaStream_t st = cx.stream();
+  const long long ec = (long long)m * n;
+  if (da < 0 || db < 0 || d <= 0) return zero_out(C, ec, 0, C.len, st);
+  A.len = da + 1;
+  B.len = db + 1;
+  if (exact) {
+    // true slice: cyclic length covering the whole product, window at c
+    if (c > da + db) return zero_out(C, ec, 0, C.len, st);
+    const long long plen = (long long)da + db + 1;
+    const int logn = ceil_log2_min1(plen);
+    OutRef C2 = C;
+    long long w = d < C.len ? d : C.len;
+    if (w > plen - c) w = plen - c;  // positions past the product are zero
+    C2.len = (int)w;
+    FPM_TRY(cyclic_product(cx, p, m, k, n, A, B, logn, c, C2));
+    return zero_out(C, ec, C2.len, C.len, st);
+  }
+  // reference dispatch (polmat.py:490-497)
+  const long long need = (long long)da + d + 1;
+  const int log_len = ceil_log2_min1(need);
+  const long long Nn = 1LL << (log_len < 62 ? log_len : 62);
+  const bool wrap_ok = c + Nn > (long long)da + db;
+  const int two = h_two_adicity(p);
+  if (need >= 64 && log_len <= two && wrap_ok) {
+    // matrix cyclic path: B folded mod x^N, window at (c + t) mod N
+    OutRef C2 = C;
+    C2.len = d < C.len ? d : C.len;
+    if (log_len < kMinLogN) {
+      // cannot happen (need >= 64) -- kept for clarity
+      set_last_error("internal: cyclic length below minimum");
+      return kInvalidArgument;
+    }
+    FPM_TRY(cyclic_product(cx, p, m, k, n, A, B, log_len, c, C2));
+    return zero_out(C, ec, C2.len, C.len, st);
+  }
+  if (need < 64) {
+    // every entry pair takes the schoolbook branch of upoly._middle
+    // (la*d <= need^2/4 < 1024): the result is the exact slice
+    return polmat_middle(cx, p, m, k, n, A, B, da, db, c, d, 1, C);
+  }
+  // generic entrywise semantics (small two-adicity primes): direct kernel
+  MiddleEntryArgs ma{};
+  ma.A = A.ptr; ma.B = B.ptr; ma.out = C.ptr;
+  ma.in64 = A.is64; ma.out64 = C.is64;
+  if (A.is64 != B.is64 || A.is64 != C.is64 || A.stride != A.len || B.stride != B.len ||
+      C.stride != d || C.len != d) {
+    set_last_error("entrywise middle product needs dense operands of one element width");
+    return kInvalidArgument;
+  }
+  ma.m = m; ma.k = k; ma.n = n; ma.la = (int)A.stride; ma.lb = (int)B.stride;
+  ma.c = c; ma.d = d;
+  CrtArgs tmp{};
+  crt_prepare(tmp, kCrtPrimes, 1, p);
+  ma.P = p; ma.Pni = tmp.Pni;
+  {
+    const u128 R = ((u128)1 << 64) % p;
+    ma.R2 = (uint64_t)(R * R % p);
+  }
+  ma.two_adicity = two;
+  return launch_middle_entrywise(ma, st);
+}
+
+}  // namespace fpm

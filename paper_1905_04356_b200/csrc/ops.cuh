@@ -1,0 +1,50 @@
+// ops.cuh -- polynomial-matrix products built from the kernels:
+//   eval (forward NTT) -> pointwise mod-p matrix products -> interpolate
+//   (inverse NTT) [-> CRT for moduli outside the direct 31-bit NTT range].
+//
+// Reference counterparts: polmat._pm_mul_ntt (polmat.py:290-308) and the
+// cyclic branch of polmat._pm_middle (polmat.py:493-522); the dispatch
+// wrappers mirror pm_mul (polmat.py:447-467) and _pm_middle (:484-536).
+#pragma once
+#include "runtime.cuh"
+
+namespace fpm {
+
+// dense polynomial matrix operand: entry e's coefficients at
+// ptr + e*stride (elements), `len` coefficients used (rest implied zero)
+struct MatRef {
+  const void* ptr;
+  int is64;
+  long long stride;
+  int len;
+};
+
+struct OutRef {
+  void* ptr;
+  int is64;
+  long long stride;
+  int len;  // coefficients written per entry
+};
+
+// C = window of (A * fold_N(B)) mod (x^N - 1) over F_p:
+//   C[e][t] = cyc[(off + t) mod N], t < out.len, N = 2^logn.
+// With N >= len(A) + len(B) - 1 and no fold this is the plain product.
+int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                   int logn, long long off, OutRef C);
+
+// full product A*B (length la + lb - 1, truncated/padded to C.len)
+int polmat_mul(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B, OutRef C);
+
+// reference `_pm_middle(A, B, c, d)` semantics (incl. its cyclic fold) when
+// exact == 0; the true coefficient slice [c, c+d) of A*B when exact == 1.
+// da/db: matrix degrees of A and B (-1 for zero matrices).
+int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                  int da, int db, long long c, int d, int exact, OutRef C);
+
+// smallest logn with 2^logn >= need, at least 1 (polmat.py:294)
+int ceil_log2_min1(long long need);
+
+// device-side degree of a dense matrix (max trimmed length - 1), synchronous
+int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L, int* deg);
+
+}  // namespace fpm

@@ -1,0 +1,19 @@
+// pmbasis.cuh -- GPU-resident M-Basis / PM-Basis (appint.py:143-196).
+#pragma once
+#include "ops.cuh"
+
+namespace fpm {
+
+// mbasis(F.truncate(order), order, s): F dense (m x n, entry stride fs, lf
+// coefficients used).  P out: m x m entries with stride ps (>= order+1),
+// all ps coefficients written (zeros past *lp).  rdeg_out: host, optional.
+int mbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, long long fs,
+               int lf, int order, const int64_t* shift, void* P, long long ps, int* lp,
+               int64_t* rdeg_out);
+
+// divide-and-conquer pmbasis with base threshold T (config.PMBASIS_BASE_ORDER)
+int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, long long fs,
+                int lf, int order, const int64_t* shift, int T, void* P, long long ps, int* lp,
+                int64_t* rdeg_out);
+
+}  // namespace fpm

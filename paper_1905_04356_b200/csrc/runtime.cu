@@ -1,0 +1,257 @@
+// runtime.cu -- context, allocator, plan cache, error string, host number theory.
+#include "runtime.cuh"
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace fpm {
+
+std::atomic<long long> g_launch_count{0};
+
+static thread_local char g_err[1024] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_err; }
+
+// ---- number theory (host) ---------------------------------------------------
+bool h_is_prime(uint64_t n) {
+  // deterministic Miller-Rabin for n < 2^64 (same witness set as modring.py:20)
+  if (n < 2) return false;
+  static const uint64_t W[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (uint64_t q : W)
+    if (n % q == 0) return n == q;
+  uint64_t d = n - 1;
+  int r = 0;
+  while ((d & 1) == 0) { d >>= 1; ++r; }
+  for (uint64_t a : W) {
+    uint64_t x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 0; i < r - 1; ++i) {
+      x = h_mulmod(x, x, n);
+      if (x == n - 1) { comp = false; break; }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+int h_two_adicity(uint64_t p) {
+  uint64_t m = p - 1;
+  int k = 0;
+  while (m && (m & 1) == 0) { m >>= 1; ++k; }
+  return k;
+}
+uint64_t h_ntt_root(uint64_t p) {
+  const int k = h_two_adicity(p);
+  uint64_t a = 2;
+  while (h_powmod(a, (p - 1) / 2, p) == 1) ++a;
+  return h_powmod(a, (p - 1) >> k, p);
+}
+
+// ---- context ----------------------------------------------------------------
+Context::Context(int device) : device_(device) {}
+
+int Context::init() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    set_last_error("no CUDA device available");
+    return kNoDevice;
+  }
+  if (device_ < 0 || device_ >= n) {
+    set_last_error("device %d out of range (%d devices)", device_, n);
+    return kInvalidArgument;
+  }
+  FPM_CUDA_TRY(cudaSetDevice(device_));
+  cudaDeviceProp prop;
+  FPM_CUDA_TRY(cudaGetDeviceProperties(&prop, device_));
+  if (prop.major < 10) {
+    set_last_error("device %d is sm_%d%d; this library is built for sm_100a", device_,
+                   prop.major, prop.minor);
+    return kNoDevice;
+  }
+  FPM_CUDA_TRY(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  own_stream_ = true;
+  return kOk;
+}
+
+Context::~Context() {
+  cudaSetDevice(device_);
+  if (stream_) cudaStreamSynchronize(stream_);
+  for (auto& kv : free_) cudaFree(kv.second);
+  for (auto& kv : used_) cudaFree(kv.first);
+  for (auto& kv : plans_) {
+    cudaFree(kv.second.tw);
+    cudaFree(kv.second.itw);
+  }
+  if (pinned_) cudaFreeHost(pinned_);
+  if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+}
+
+int Context::set_stream(cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (s == stream_) return kOk;
+  // pooled blocks were last used in the old stream's order: drain it first
+  if (stream_) FPM_CUDA_TRY(cudaStreamSynchronize(stream_));
+  if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+  own_stream_ = false;
+  stream_ = s;
+  return kOk;
+}
+
+int Context::alloc(size_t bytes, void** out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  bytes = (bytes + 255) & ~(size_t)255;
+  auto it = free_.lower_bound(bytes);
+  if (it != free_.end() && it->first <= 2 * bytes + (1 << 20)) {
+    *out = it->second;
+    used_[it->second] = it->first;
+    free_.erase(it);
+    return kOk;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    // release cached blocks and retry once
+    cudaStreamSynchronize(stream_);
+    for (auto& kv : free_) cudaFree(kv.second);
+    free_.clear();
+    e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_last_error("cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+      return kOutOfMemory;
+    }
+  }
+  used_[p] = bytes;
+  *out = p;
+  return kOk;
+}
+
+void Context::release(void* ptr) {
+  std::lock_guard<std::mutex> lk(mu_);
+  auto it = used_.find(ptr);
+  if (it == used_.end()) return;
+  free_.emplace(it->second, ptr);
+  used_.erase(it);
+}
+
+int Context::pinned(size_t bytes, void** out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (pinned_bytes_ < bytes) {
+    if (pinned_) {
+      FPM_CUDA_TRY(cudaStreamSynchronize(stream_));
+      cudaFreeHost(pinned_);
+      pinned_ = nullptr;
+    }
+    FPM_CUDA_TRY(cudaMallocHost(&pinned_, bytes));
+    pinned_bytes_ = bytes;
+  }
+  *out = pinned_;
+  return kOk;
+}
+
+int Context::plan(uint32_t p, int logn, const Plan** out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  auto key = std::make_pair(p, logn);
+  auto it = plans_.find(key);
+  if (it != plans_.end()) {
+    *out = &it->second;
+    return kOk;
+  }
+  const int k = h_two_adicity(p);
+  if (logn > k) {
+    set_last_error("p=%u supports transforms up to length 2^%d, not 2^%d", p, k, logn);
+    return kOrderTooSmall;
+  }
+  const size_t N = (size_t)1 << logn, H = N / 2;
+  // omega = root^(2^(k - logn)) (modring.py:233)
+  const uint64_t omega = h_powmod(h_ntt_root(p), (uint64_t)1 << (k - logn), p);
+  const uint64_t iomega = h_invmod(omega, p);
+  std::vector<uint2> tw(H), itw(H);
+  uint64_t w = 1, iw = 1;
+  for (size_t e = 0; e < H; ++e) {
+    tw[e] = make_uint2((uint32_t)w, h_shoup((uint32_t)w, p));
+    itw[e] = make_uint2((uint32_t)iw, h_shoup((uint32_t)iw, p));
+    w = h_mulmod(w, omega, p);
+    iw = h_mulmod(iw, iomega, p);
+  }
+  Plan pl;
+  pl.p = p;
+  pl.logn = logn;
+  FPM_CUDA_TRY(cudaMalloc(&pl.tw, H * sizeof(uint2)));
+  FPM_CUDA_TRY(cudaMalloc(&pl.itw, H * sizeof(uint2)));
+  FPM_CUDA_TRY(cudaMemcpy(pl.tw, tw.data(), H * sizeof(uint2), cudaMemcpyHostToDevice));
+  FPM_CUDA_TRY(cudaMemcpy(pl.itw, itw.data(), H * sizeof(uint2), cudaMemcpyHostToDevice));
+  pl.ninv = (uint32_t)h_invmod(N % p, p);
+  pl.ninv_sh = h_shoup(pl.ninv, p);
+  auto res = plans_.emplace(key, pl);
+  *out = &res.first->second;
+  return kOk;
+}
+
+cudaEvent_t Context::get_event() {
+  if (!ev_free_.empty()) {
+    cudaEvent_t e = ev_free_.back();
+    ev_free_.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void Context::profile_enable(bool on) {
+  for (auto& s : stages_) {
+    ev_free_.push_back(s.a);
+    ev_free_.push_back(s.b);
+  }
+  stages_.clear();
+  profiling_ = on;
+}
+
+int Context::stage_mark(const char* name, bool begin) {
+  if (begin) {
+    StageRec r{name, get_event(), get_event()};
+    FPM_CUDA_TRY(cudaEventRecord(r.a, stream_));
+    stages_.push_back(r);
+  } else {
+    for (auto it = stages_.rbegin(); it != stages_.rend(); ++it) {
+      // close the innermost open stage (b not yet recorded is marked by name)
+      if (it->name) {
+        FPM_CUDA_TRY(cudaEventRecord(it->b, stream_));
+        break;
+      }
+    }
+  }
+  return kOk;
+}
+
+int Context::profile_get(int i, const char** name, float* ms) {
+  if (i < 0 || i >= (int)stages_.size()) return kInvalidArgument;
+  FPM_CUDA_TRY(cudaEventSynchronize(stages_[i].b));
+  FPM_CUDA_TRY(cudaEventElapsedTime(ms, stages_[i].a, stages_[i].b));
+  *name = stages_[i].name;
+  return kOk;
+}
+
+int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
+  const Plan* pl = nullptr;
+  FPM_TRY(plan(p, logn, &pl));
+  out->p = p;
+  out->c32 = (uint32_t)(((uint64_t)1 << 32) % p);
+  out->mu = (uint64_t)((((u128)1) << 64) / p);
+  out->ninv = pl->ninv;
+  out->ninv_sh = pl->ninv_sh;
+  out->tw = pl->tw;
+  out->itw = pl->itw;
+  return kOk;
+}
+
+}  // namespace fpm

@@ -1,0 +1,103 @@
+// runtime.cuh -- per-context native runtime: stream, caching device
+// allocator, pinned staging, and the NTT plan (twiddle table) cache.
+#pragma once
+#include <map>
+#include <mutex>
+#include <vector>
+#include <atomic>
+#include "common.cuh"
+
+namespace fpm {
+
+struct Plan {
+  uint32_t p = 0;
+  int logn = 0;
+  uint2* tw = nullptr;   // device, N/2 entries
+  uint2* itw = nullptr;  // device, N/2 entries
+  uint32_t ninv = 0, ninv_sh = 0;
+};
+
+class Context {
+ public:
+  explicit Context(int device);
+  ~Context();
+  int init();
+  int device() const { return device_; }
+  cudaStream_t stream() const { return stream_; }
+  int set_stream(cudaStream_t s);
+
+  // stream-ordered caching allocator (blocks are reused in stream order)
+  int alloc(size_t bytes, void** out);
+  void release(void* ptr);
+  // pinned host staging buffer of at least `bytes`
+  int pinned(size_t bytes, void** out);
+
+  int plan(uint32_t p, int logn, const Plan** out);
+  int prime_const(uint32_t p, int logn, PrimeConst* out);
+
+  // stage profiling (tracing subsystem): CUDA events around each kernel
+  // stage on the context stream, read back by fpm_profile_get
+  void profile_enable(bool on);
+  bool profiling() const { return profiling_; }
+  int stage_mark(const char* name, bool begin);
+  int profile_count() const { return (int)stages_.size(); }
+  int profile_get(int i, const char** name, float* ms);
+
+ private:
+  struct StageRec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  bool profiling_ = false;
+  std::vector<StageRec> stages_;
+  std::vector<cudaEvent_t> ev_free_;
+  cudaEvent_t get_event();
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  bool own_stream_ = false;
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> used_;
+  std::map<std::pair<uint32_t, int>, Plan> plans_;
+  void* pinned_ = nullptr;
+  size_t pinned_bytes_ = 0;
+};
+
+// RAII stage timer: no-op unless the context is profiling
+class StageTimer {
+ public:
+  StageTimer(Context& cx, const char* name) : cx_(cx), on_(cx.profiling()) {
+    if (on_) cx_.stage_mark(name, true);
+  }
+  ~StageTimer() {
+    if (on_) cx_.stage_mark(nullptr, false);
+  }
+
+ private:
+  Context& cx_;
+  bool on_;
+};
+
+// RAII workspace block from the context pool
+class Workspace {
+ public:
+  explicit Workspace(Context& cx) : cx_(cx) {}
+  ~Workspace() {
+    for (void* p : blocks_) cx_.release(p);
+  }
+  template <typename T>
+  int get(size_t count, T** out) {
+    void* p = nullptr;
+    int s = cx_.alloc(count * sizeof(T) + 16, &p);
+    if (s != kOk) return s;
+    blocks_.push_back(p);
+    *out = (T*)p;
+    return kOk;
+  }
+
+ private:
+  Context& cx_;
+  std::vector<void*> blocks_;
+};
+
+}  // namespace fpm
