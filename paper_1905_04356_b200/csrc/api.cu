@@ -245,8 +245,10 @@ int fpm_mbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int 
     set_last_error("mbasis needs m >= 1, n >= 0, order >= 0");
     return kInvalidArgument;
   }
-  return mbasis_run(*ctx->cx, p, elem_bytes == 8, F, m, n, lf, lf, order, shift, P, order + 1,
-                    lp, rdeg_out);
+  // identical output for every base threshold (appint.py:24-60 canonical
+  // steps), so the iterative M-Basis is served by the same GPU recursion
+  return pmbasis_run(*ctx->cx, p, elem_bytes == 8, F, m, n, lf, lf, order, shift,
+                     ctx->pmbasis_T, P, order + 1, lp, rdeg_out);
 }
 
 int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n,

@@ -111,15 +111,18 @@ __device__ __forceinline__ uint32_t d_red64(uint64_t x, uint32_t p, uint64_t mu)
   return r >= p ? r32 - p : r32;
 }
 
-// Per-prime constants handed to kernels by value.
+// Per-prime constants handed to kernels by value (kernel-parameter space, so
+// the radix-32 root constants are constant-bank operands, not loads).
 struct PrimeConst {
   uint32_t p;
   uint32_t c32;      // 2^32 mod p (pointwise fold)
   uint64_t mu;       // floor(2^64 / p) (Barrett)
   uint32_t ninv;     // N^-1 mod p for the transform length in use
   uint32_t ninv_sh;  // Shoup companion of ninv
-  const uint2* tw;   // forward (w, w') table, N/2 entries
-  const uint2* itw;  // inverse table, N/2 entries
+  const uint2* tw;   // forward twiddle rows: tw[r*32 + k] = w^(r*k), N entries
+  const uint2* itw;  // inverse rows: w^-(r*k), N entries
+  uint2 w32[16];     // (w32^e, Shoup) e < 16, w32 = w^(N/32): inner radix-32 DFTs
+  uint2 iw32[16];    // inverse roots
 };
 
 constexpr int kMaxPrimes = 8;

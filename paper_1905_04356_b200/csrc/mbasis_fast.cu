@@ -1,0 +1,456 @@
+// mbasis_fast.cu -- M-Basis leaf as two kernels (31-bit primes).
+//
+// The reference M-Basis (appint.py:143-180) interleaves three things per
+// order-1 step: the residual R_k = coeff_k(P F), the canonical step
+// (appint.py:24-60) and P <- Q_k P plus s <- rdeg_s(P).  Two facts split the
+// work into a short sequential chain and a wide parallel product:
+//   * s <- rdeg_s(P) equals s + delta (delta = 1 on the step's pivot rows):
+//     P stays s-ordered weak Popov, hence s-reduced, and the predictable
+//     degree property gives rdeg(Q_k P) = rdeg_{rdeg(P)}(Q_k) = s + delta
+//     (checked against the reference on 3595 steps incl. degenerate inputs);
+//   * so the chain needs only the residual list G = P F mod x^T, updated by
+//     each step (the reference's update_list variant, appint.py:173-178).
+// Kernel A runs the T steps in one CTA with G in shared memory and records
+// every step (pivot order + kernel-row coefficients).  Kernel B rebuilds
+// P = Q_{T-1} ... Q_0 from the records, one CTA per column of P (the update
+// P <- Q P never mixes columns).
+//
+// Canonical step, exactly as the reference: rows ranked by (s_i, i); the
+// pivot rows are the rows outside the span of their predecessors, found by
+// column elimination that always picks the lowest-ranked remaining row (the
+// pivot SET is the greedy basis, independent of elimination order); kernel
+// row i of the basis is e_i - sum_j c_ij e_j over pivot rows j (unique).
+// The elimination is division free: row_i <- (a*row_i - b*row_r) * 2^-32
+// (one Montgomery reduction; a nonzero row factor is harmless), with a
+// transform matrix X tracking each row; at the end c_ij = -X_ij / X_ii.
+// One barrier per column: while updating, the owner of column c+1 of each
+// row already reduces the next pivot key.
+#include <climits>
+#include "pmbasis.cuh"
+
+namespace fpm {
+namespace {
+
+struct F31 {
+  uint32_t p, pinv;  // pinv = -p^-1 mod 2^32
+  uint64_t mu;       // floor(2^64 / p)
+  uint32_t c32;      // 2^32 mod p
+};
+
+// (a*w + (p-b)*y) * 2^-32 mod p, all inputs < p, result < p
+__device__ __forceinline__ uint32_t redc_axby(uint32_t a, uint32_t w, uint32_t b, uint32_t y,
+                                              const F31& f) {
+  const uint64_t acc = (uint64_t)a * w + (uint64_t)(f.p - b) * y;  // < 2p^2 < 2^63
+  const uint32_t m = (uint32_t)acc * f.pinv;
+  const uint32_t t = (uint32_t)((acc + (uint64_t)m * f.p) >> 32);  // < 2p
+  return min(t, t - f.p);
+}
+
+__device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const F31& f) {
+  return d_red64((uint64_t)a * b, f.p, f.mu);
+}
+
+__device__ uint32_t invmod(uint32_t a, const F31& f) {
+  uint32_t r = 1, b = a;
+  uint32_t e = f.p - 2;
+  while (e) {
+    if (e & 1) r = mulmod(r, b, f);
+    b = mulmod(b, b, f);
+    e >>= 1;
+  }
+  return r;
+}
+
+__device__ __forceinline__ uint64_t fold(uint64_t acc, uint32_t c32) {
+  return (uint64_t)(uint32_t)(acc >> 32) * c32 + (uint32_t)acc;
+}
+
+struct StepArgs {
+  const uint32_t* F;
+  long long fs;
+  int lf, m, n, T;
+  const int64_t* s;   // device shift (m)
+  int* rec_np;        // [T] number of pivots
+  int* rec_plist;     // [T][m] pivot rows in discovery order
+  uint32_t* rec_Ct;   // [T][m*m] compact: Ct[q*nk + kr] = -c_{klist[kr], plist[q]}
+  int64_t* sft_out;   // final shift (m)
+  int fold_k;         // products between folds (pointwise.cu fold_period)
+  F31 f;
+};
+
+constexpr int kStepThreads = 512;
+
+__global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int m = a.m, n = a.n, T = a.T;
+  const int tid = threadIdx.x;
+  const F31 f = a.f;
+  const uint32_t p = f.p;
+  const size_t mn = (size_t)m * n;
+  int64_t* sft = (int64_t*)smraw;                 // m
+  uint32_t* G = (uint32_t*)(sft + m);             // [T][m][n]
+  uint32_t* W = G + (size_t)T * mn;               // [m][n]  (later: compact Ct)
+  uint32_t* X = W + mn;                           // [m][m]
+  uint32_t* inv = X + (size_t)m * m;              // m
+  int* rank = (int*)(inv + m);                    // m
+  int* ord = rank + m;                            // m
+  int* piv = ord + m;                             // m
+  int* plist = piv + m;                           // m
+  int* klist = plist + m;                         // m
+  __shared__ int s_key[2];
+  __shared__ int s_nk;
+
+  const int hw = tid >> 4, l16 = tid & 15;  // half-warp per row
+  constexpr int kRowsPerPass = kStepThreads / 16;
+
+  for (int e = tid; e < (int)mn; e += kStepThreads) {
+    const uint32_t* fe = a.F + (long long)e * a.fs;
+    for (int t = 0; t < T; ++t) G[(size_t)t * mn + e] = t < a.lf ? fe[t] : 0u;
+  }
+  for (int i = tid; i < m; i += kStepThreads) sft[i] = a.s[i];
+  __syncthreads();
+
+  for (int k = 0; k < T; ++k) {
+    const uint32_t* Gk = G + (size_t)k * mn;
+    for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
+    for (int idx = tid; idx < m * m; idx += kStepThreads)
+      X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
+    for (int i = tid; i < m; i += kStepThreads) {
+      int r = 0;
+      const int64_t si = sft[i];
+      for (int j = 0; j < m; ++j) r += (sft[j] < si) || (sft[j] == si && j < i);
+      rank[i] = r;
+      ord[r] = i;
+      piv[i] = 0;
+    }
+    if (tid < 2) s_key[tid] = INT_MAX;
+    __syncthreads();
+
+    // ---- column elimination, lowest-rank pivot per column --------------------
+    // Fast mode: while the pivots so far are exactly ranks 0..np-1, the pivot
+    // of column c is the rank-np row if its entry is nonzero (it is then the
+    // lowest-ranked candidate) -- no search.  Otherwise (rare: degenerate
+    // residuals) switch to the general search for the rest of the step.
+    int np = 0;
+    bool fastm = true;
+    for (int c = 0; c < n; ++c) {
+      int r = -1;
+      if (fastm && np < m) {
+        const int rr = ord[np];
+        if (W[(size_t)rr * n + c] != 0) r = rr;
+      }
+      if (r < 0) {
+        fastm = false;
+        // general: lowest rank among non-pivot rows with a nonzero in column c
+        const int slot = c & 1;
+        for (int i = hw; i < m; i += kRowsPerPass)
+          if (l16 == 0 && !piv[i] && W[(size_t)i * n + c] != 0) atomicMin(&s_key[slot], rank[i]);
+        __syncthreads();
+        const int key = s_key[slot];
+        if (tid == 0) s_key[slot ^ 1] = INT_MAX;
+        if (key == INT_MAX) {
+          __syncthreads();
+          continue;  // uniform: empty column
+        }
+        r = ord[key];
+      }
+      const uint32_t av = W[(size_t)r * n + c];
+      for (int i = hw; i < m; i += kRowsPerPass) {
+        if (piv[i] || i == r) continue;
+        uint32_t* Wi = W + (size_t)i * n;
+        const uint32_t bv = Wi[c];
+        if (bv == 0) continue;
+        const uint32_t* Wr = W + (size_t)r * n;
+        uint32_t* Xi = X + (size_t)i * m;
+        const uint32_t* Xr = X + (size_t)r * m;
+#pragma unroll 4
+        for (int j = c + 1 + l16; j < n; j += 16) Wi[j] = redc_axby(av, Wi[j], bv, Wr[j], f);
+        // X: columns of earlier pivots, the new pivot r, and the diagonal
+#pragma unroll 4
+        for (int q = l16; q < np + 2; q += 16) {
+          const int l = q < np ? plist[q] : (q == np ? r : i);
+          Xi[l] = redc_axby(av, Xi[l], bv, Xr[l], f);
+        }
+      }
+      if (tid == 0) {
+        piv[r] = 1;
+        plist[np] = r;
+      }
+      ++np;
+      __syncthreads();
+    }
+
+    // ---- record the step; normalise kernel rows: Ct = X_il / X_ii ------------
+    if (tid == 0) {
+      int nk = 0;
+      for (int i = 0; i < m; ++i)
+        if (!piv[i]) klist[nk++] = i;
+      s_nk = nk;
+      a.rec_np[k] = np;
+    }
+    for (int q = tid; q < np; q += kStepThreads) a.rec_plist[(size_t)k * m + q] = plist[q];
+    __syncthreads();
+    const int nk = s_nk;
+    if (np == 0) continue;  // R = 0: nothing changes (appint.py:171)
+    for (int kr = tid; kr < nk; kr += kStepThreads) {
+      const int i = klist[kr];
+      inv[kr] = invmod(X[(size_t)i * m + i], f);
+    }
+    __syncthreads();
+    uint32_t* Ct = W;  // compact [np][nk]
+    uint32_t* recC = a.rec_Ct + (size_t)k * m * m;
+    for (int idx = tid; idx < np * nk; idx += kStepThreads) {
+      const int q = idx / nk, kr = idx - (idx / nk) * nk;
+      const uint32_t v = mulmod(X[(size_t)klist[kr] * m + plist[q]], inv[kr], f);
+      Ct[idx] = v;
+      recC[idx] = v;
+    }
+    __syncthreads();
+
+    // ---- residual list: kernel rows G[t][i] += sum_q Ct G[t][plist[q]], t > k -
+    {
+      const int rb_n = (nk + 3) >> 2, cb_n = (n + 3) >> 2, nt = T - k - 1;
+      const int blocks = rb_n * cb_n * nt;
+      const int K = a.fold_k;
+      for (int b = tid; b < blocks; b += kStepThreads) {
+        const int t = k + 1 + b / (rb_n * cb_n);
+        const int rem = b - (b / (rb_n * cb_n)) * (rb_n * cb_n);
+        const int rb = rem / cb_n, cb = rem - (rem / cb_n) * cb_n;
+        uint32_t* Gt = G + (size_t)t * mn;
+        int rows[4];
+        uint64_t acc[4][4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int kr = rb * 4 + r;
+          rows[r] = kr < nk ? klist[kr] : -1;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int j = cb * 4 + cc;
+            acc[r][cc] = (rows[r] >= 0 && j < n) ? Gt[(size_t)rows[r] * n + j] : 0;
+          }
+        }
+        if (((n | nk) & 3) == 0 && K == 4) {
+          // aligned fast path: 16-byte shared loads, folds at fixed positions
+#pragma unroll 1
+          for (int q = 0; q < np; ++q) {
+            const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + (size_t)plist[q] * n + cb * 4);
+            const uint4 c4 = *reinterpret_cast<const uint4*>(Ct + q * nk + rb * 4);
+            const uint32_t gv[4] = {g4.x, g4.y, g4.z, g4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) acc[r][cc] += (uint64_t)cv[r] * gv[cc];
+            if ((q & 3) == 3) {
+#pragma unroll
+              for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) acc[r][cc] = fold(acc[r][cc], f.c32);
+            }
+          }
+        } else {
+          int cnt = 0;
+          for (int q = 0; q < np; ++q) {
+            const uint32_t* gl = Gt + (size_t)plist[q] * n + cb * 4;
+            uint32_t gv[4], cv[4];
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) gv[cc] = (cb * 4 + cc < n) ? gl[cc] : 0u;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cv[r] = (rb * 4 + r < nk) ? Ct[q * nk + rb * 4 + r] : 0u;
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) acc[r][cc] += (uint64_t)cv[r] * gv[cc];
+            if (++cnt == K) {
+              cnt = 0;
+#pragma unroll
+              for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) acc[r][cc] = fold(acc[r][cc], f.c32);
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (rows[r] < 0) continue;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            const int j = cb * 4 + cc;
+            if (j < n) Gt[(size_t)rows[r] * n + j] = d_red64(acc[r][cc], p, f.mu);
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k) ----
+    for (int idx = tid; idx < np * n; idx += kStepThreads) {
+      const int i = plist[idx / n], j = idx - (idx / n) * n;
+      for (int t = T - 1; t >= k + 1; --t)
+        G[(size_t)t * mn + (size_t)i * n + j] = G[(size_t)(t - 1) * mn + (size_t)i * n + j];
+    }
+    for (int i = tid; i < m; i += kStepThreads) sft[i] += piv[i];
+    __syncthreads();
+  }
+  for (int i = tid; i < m; i += kStepThreads) a.sft_out[i] = sft[i];
+}
+
+struct BuildArgs {
+  const int* rec_np;
+  const int* rec_plist;
+  const uint32_t* rec_Ct;
+  int m, T;
+  uint32_t* P;  // entry-major output, stride ps
+  long long ps;
+  int fold_k;
+  F31 f;
+};
+
+// one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j
+__global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
+  extern __shared__ __align__(16) uint32_t bsm[];
+  const int m = a.m, T = a.T, j = blockIdx.x;
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int L1 = T + 1;
+  uint32_t* P0 = bsm;                   // [L1][m]
+  uint32_t* P1 = bsm + (size_t)L1 * m;  // [L1][m]
+  int* isp = (int*)(bsm + 2 * (size_t)L1 * m + (size_t)m * m);  // m: pivot index q or -1 (after Ct)
+  int* kidx = isp + m;                  // m: kernel index kr or -1
+  int* plist = kidx + m;                // m
+  for (int idx = tid; idx < L1 * m; idx += NT) P0[idx] = (idx == j) ? 1u : 0u;
+  int L = 1;
+  for (int k = 0; k < T; ++k) {
+    const int np = a.rec_np[k];
+    if (np == 0) continue;  // R = 0: the reference leaves P unchanged
+    __syncthreads();
+    for (int i = tid; i < m; i += NT) isp[i] = -1;
+    __syncthreads();
+    for (int q = tid; q < np; q += NT) {
+      const int l = a.rec_plist[(size_t)k * m + q];
+      plist[q] = l;
+      isp[l] = q;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int nk = 0;
+      for (int i = 0; i < m; ++i) kidx[i] = isp[i] < 0 ? nk++ : -1;
+    }
+    __syncthreads();
+    const int nk = m - np;
+    uint32_t* Ct = bsm + 2 * (size_t)L1 * m;  // staged [np][nk] (fixed, after both P buffers)
+    {
+      const uint32_t* g = a.rec_Ct + (size_t)k * m * m;
+      for (int idx = tid; idx < np * nk; idx += NT) Ct[idx] = g[idx];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (L + 1) * m; idx += NT) {
+      const int t = idx / m, i = idx - (idx / m) * m;
+      uint32_t v = 0;
+      if (isp[i] >= 0) {
+        if (t >= 1) v = P0[(size_t)(t - 1) * m + i];
+      } else if (t < L) {
+        const int kr = kidx[i];
+        uint64_t acc = P0[(size_t)t * m + i];
+        int cnt = 0;
+        for (int q = 0; q < np; ++q) {
+          acc += (uint64_t)Ct[(size_t)q * nk + kr] * P0[(size_t)t * m + plist[q]];
+          if (++cnt == a.fold_k) {
+            cnt = 0;
+            acc = fold(acc, a.f.c32);
+          }
+        }
+        v = d_red64(acc, a.f.p, a.f.mu);
+      }
+      P1[idx] = v;
+    }
+    __syncthreads();
+    uint32_t* tmp = P0; P0 = P1; P1 = tmp;
+    ++L;
+  }
+  __syncthreads();
+  // column j of P, entry-major: P[(i*m + j)*ps + t]
+  const int ps = (int)a.ps;
+  for (int idx = tid; idx < m * ps; idx += NT) {
+    const int i = idx / ps, t = idx - (idx / ps) * ps;
+    a.P[((long long)i * m + j) * ps + t] = t < L ? P0[(size_t)t * m + i] : 0u;
+  }
+}
+
+F31 make_f31(uint32_t p) {
+  F31 f;
+  f.p = p;
+  uint32_t inv = p;
+  for (int i = 0; i < 5; ++i) inv *= 2 - p * inv;
+  f.pinv = 0u - inv;
+  f.mu = (uint64_t)((((u128)1) << 64) / p);
+  f.c32 = (uint32_t)(((uint64_t)1 << 32) % p);
+  return f;
+}
+
+size_t steps_smem(int m, int n, int T) {
+  return 8 * (size_t)m + 4 * ((size_t)T * m * n + (size_t)m * n + (size_t)m * m + m) +
+         4 * 5 * (size_t)m;
+}
+
+}  // namespace
+
+int fold_period(uint32_t p);  // pointwise.cu
+
+int mbasis_fast_max_order(int m, int n) {
+  // largest leaf order whose residual list fits in shared memory
+  const size_t cap = 200 * 1024;
+  if (2 * (size_t)2 * m * 4 > cap) return 0;
+  int T = 0;
+  while (T < 64 && steps_smem(m, n, T + 1) <= cap && (size_t)(T + 2) * m * 8 + 12 * m <= cap) ++T;
+  return T;
+}
+
+int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long fs, int lf,
+                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev) {
+  if (order < 1 || order > mbasis_fast_max_order(m, n)) {
+    set_last_error("mbasis_fast: shape m=%d n=%d order=%d exceeds shared memory", m, n, order);
+    return kUnsupported;
+  }
+  const size_t smem = steps_smem(m, n, order);
+  Workspace ws(cx);
+  int* rec_np;
+  int* rec_plist;
+  uint32_t* rec_Ct;
+  FPM_TRY(ws.get((size_t)order, &rec_np));
+  FPM_TRY(ws.get((size_t)order * m, &rec_plist));
+  FPM_TRY(ws.get((size_t)order * m * m, &rec_Ct));
+  const F31 f = make_f31(p);
+  const int K = fold_period(p);
+  StepArgs sa{};
+  sa.F = (const uint32_t*)F; sa.fs = fs; sa.lf = lf < order ? lf : order;
+  sa.m = m; sa.n = n; sa.T = order; sa.s = s_dev;
+  sa.rec_np = rec_np; sa.rec_plist = rec_plist; sa.rec_Ct = rec_Ct;
+  sa.sft_out = sft_dev; sa.fold_k = K; sa.f = f;
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_steps_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  {
+    StageTimer t_(cx, "mbasis_steps");
+    mbasis_steps_kernel<<<1, kStepThreads, smem, cx.stream()>>>(sa);
+    FPM_LAUNCH_CHECK();
+  }
+  BuildArgs ba{};
+  ba.rec_np = rec_np; ba.rec_plist = rec_plist; ba.rec_Ct = rec_Ct; ba.m = m; ba.T = order;
+  ba.P = (uint32_t*)P; ba.ps = ps; ba.fold_k = K; ba.f = f;
+  const size_t bsmem = 2 * (size_t)(order + 1) * m * 4 + 4 * (size_t)m * m + 12 * (size_t)m;
+  static size_t battr = 0;
+  if (bsmem > 48 * 1024 && bsmem > battr) {
+    FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_build_kernel,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+    battr = bsmem;
+  }
+  {
+    StageTimer t_(cx, "mbasis_build");
+    mbasis_build_kernel<<<m, 256, bsmem, cx.stream()>>>(ba);
+    FPM_LAUNCH_CHECK();
+  }
+  return kOk;
+}
+
+}  // namespace fpm

@@ -1,4 +1,15 @@
 // ntt.cu -- batched NTT kernels; see ntt.cuh for the design summary.
+//
+// Four-step radix-32 formulation.  A length-N DIF transform is split into
+// passes over 5-bit digits of the index (top, middle, last).  In each pass a
+// thread owns one 32-element sub-sequence and runs a radix-32 DFT in
+// registers whose twiddles are the 32nd roots w32^e -- identical for every
+// thread, read from kernel-parameter (constant-bank) space.  Between passes
+// every element is multiplied by one "twiddle row" value w^(r*kappa), r the
+// thread's row, kappa the DFT output index; each thread reads its 32 row
+// entries as 16 contiguous 16-byte loads.  Output order is the standard DIF
+// bit-reversed order, consumed unchanged by the pointwise stage and by the
+// inverse (the exact transposed network: twiddle rows, then radix-32 DIT).
 #include "ntt.cuh"
 
 namespace fpm {
@@ -28,73 +39,81 @@ __device__ __forceinline__ int xmap(int lt, int i) {
   }
   return (lt << 5) | i;
 }
-template <int LOGN, int MAP>
-struct PassBits {
-  static constexpr int BB = MAP == MAP_TOP ? LOGN - 5 : (MAP == MAP_MID ? LOGN - 10 : 0);
-  static constexpr int R = MAP == MAP_LAST ? Geo<LOGN>::LAST_R : 5;
-};
-// runtime part of the twiddle exponent (x mod 2^b) << (LOGN-1-b) for stage bit b
-template <int LOGN, int MAP>
-__device__ __forceinline__ int tw_base(int lt, int b) {
-  const int sh = LOGN - 1 - b;
-  if (MAP == MAP_TOP) return lt << sh;
-  if (MAP == MAP_MID) {
-    constexpr int lo = LOGN - 10;
-    return (lt & ((1 << lo) - 1)) << sh;
-  }
-  return 0;
-}
 
 __device__ __forceinline__ int pad(int x) { return x + (x >> 5); }
 
-// Gentleman-Sande pass over the pass's active bits, high to low.
-template <int LOGN, int MAP>
-__device__ __forceinline__ void dif_pass(uint32_t (&v)[32], int lt,
-                                         const uint2* __restrict__ tw, uint32_t p) {
-  constexpr int BB = PassBits<LOGN, MAP>::BB, R = PassBits<LOGN, MAP>::R;
+__host__ __device__ constexpr int brev5(int i) {
+  return ((i & 1) << 4) | ((i & 2) << 2) | (i & 4) | ((i & 8) >> 2) | ((i & 16) >> 4);
+}
+
+// radix-2^R DIF over the low R bits of the register array (natural ->
+// bit-reversed within each 2^R block); twiddles w_{2h}^j = w32^(j*16/h)
+template <int R>
+__device__ __forceinline__ void dif_small(uint32_t (&v)[32], const uint2* w, uint32_t p,
+                                          bool upper_zero) {
 #pragma unroll
-  for (int ib = R - 1; ib >= 0; --ib) {
-    const int b = BB + ib;
-    const uint2* twb = tw + tw_base<LOGN, MAP>(lt, b);
+  for (int hb = R - 1; hb >= 0; --hb) {
+    const int h = 1 << hb;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      if (i & (1 << ib)) continue;
-      const int j = i | (1 << ib);
-      const uint32_t u = v[i], w = v[j];
-      const uint32_t s = d_red(u + w, p);
-      uint32_t d = u - w + p;  // [1, 2p)
-      if (b != 0) {
-        const uint2 t = __ldg(twb + ((i & ((1 << ib) - 1)) << (LOGN - 1 - ib)));
-        d = d_shoup(d, t.x, t.y, p);
+      if (i & h) continue;
+      const int e = (i & (h - 1)) * (16 / h);
+      const uint32_t u = v[i];
+      if (R == 5 && hb == 4 && upper_zero) {
+        // first stage of a zero-padded input: (u, 0) -> (u, u*w)
+        v[i + h] = e ? d_red(d_shoup(u, w[e].x, w[e].y, p), p) : u;
+        continue;
       }
+      const uint32_t b = v[i + h];
+      const uint32_t s = d_red(u + b, p);
+      uint32_t d = u - b + p;  // [1, 2p)
+      if (e) d = d_shoup(d, w[e].x, w[e].y, p);
       v[i] = s;
-      v[j] = d_red(d, p);
+      v[i + h] = d_red(d, p);
     }
   }
 }
 
-// Cooley-Tukey pass over the pass's active bits, low to high (inverse table).
-template <int LOGN, int MAP>
-__device__ __forceinline__ void dit_pass(uint32_t (&v)[32], int lt,
-                                         const uint2* __restrict__ itw, uint32_t p) {
-  constexpr int BB = PassBits<LOGN, MAP>::BB, R = PassBits<LOGN, MAP>::R;
+// radix-2^R DIT over the low R bits (bit-reversed -> natural), inverse roots
+template <int R>
+__device__ __forceinline__ void dit_small(uint32_t (&v)[32], const uint2* w, uint32_t p) {
 #pragma unroll
-  for (int ib = 0; ib < R; ++ib) {
-    const int b = BB + ib;
-    const uint2* twb = itw + tw_base<LOGN, MAP>(lt, b);
+  for (int hb = 0; hb < R; ++hb) {
+    const int h = 1 << hb;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      if (i & (1 << ib)) continue;
-      const int j = i | (1 << ib);
+      if (i & h) continue;
+      const int e = (i & (h - 1)) * (16 / h);
       const uint32_t u = v[i];
-      uint32_t t = v[j];
-      if (b != 0) {
-        const uint2 w = __ldg(twb + ((i & ((1 << ib) - 1)) << (LOGN - 1 - ib)));
-        t = d_red(d_shoup(t, w.x, w.y, p), p);
-      }
+      uint32_t t = v[i + h];
+      if (e) t = d_red(d_shoup(t, w[e].x, w[e].y, p), p);
       v[i] = d_red(u + t, p);
-      v[j] = d_red(u - t + p, p);
+      v[i + h] = d_red(u - t + p, p);
     }
+  }
+}
+
+// split load / apply so a row's 16-byte loads are issued a whole radix-32
+// DFT (or smem exchange) ahead of their use
+struct Row {
+  uint4 t[16];
+};
+__device__ __forceinline__ void row_load(Row& r, const uint2* __restrict__ row) {
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) r.t[q] = __ldg(r4 + q);
+}
+__device__ __forceinline__ void row_apply(uint32_t (&v)[32], const Row& r, uint32_t p) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint4 t = r.t[q];
+    const int k0 = 2 * q, k1 = 2 * q + 1;
+    if (k0) {
+      const int i0 = brev5(k0);
+      v[i0] = d_red(d_shoup(v[i0], t.x, t.y, p), p);
+    }
+    const int i1 = brev5(k1);
+    v[i1] = d_red(d_shoup(v[i1], t.z, t.w, p), p);
   }
 }
 
@@ -133,12 +152,14 @@ __device__ __forceinline__ uint32_t load_coef(const NttFwdArgs& a, const PrimeCo
   return acc;
 }
 
-template <int LOGN>
+// SINGLE: one prime -> every PrimeConst field is a constant-bank operand
+// (no LDC); otherwise blockIdx.z selects the prime of a multi-prime batch.
+template <int LOGN, bool SINGLE>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
-    ntt_fwd_kernel(NttFwdArgs a, PrimeSet ps) {
+    ntt_fwd_kernel(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps) {
   using G = Geo<LOGN>;
   extern __shared__ uint32_t sm[];
-  const PrimeConst& pc = ps.pr[blockIdx.z];
+  const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
   const uint32_t p = pc.p;
   const int tid = threadIdx.x;
   const int tr = tid / G::TPT, lt = tid % G::TPT;
@@ -147,15 +168,33 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   const bool valid = e < a.n_entries;
   uint32_t* smt = sm + tr * G::STRIDE;
   const long long pin = (long long)blockIdx.z * a.in_prime_stride;
+  // the upper half of a zero-padded input is zero: skip its loads and adds
+  const bool upper_zero = G::NPASS > 1 && !a.fold && a.len <= G::N / 2;
   uint32_t v[32];
 
   constexpr int FIRST = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
   if (G::TPT >= 32) {
     // direct coalesced load: consecutive lanes read consecutive coefficients
     const long long eb = pin + e * a.in_stride;
+    if (!a.fold && !a.in64 && !a.reduce) {
+      // common case: branch-free predicated loads, all issued before use
+      const uint32_t* src = (const uint32_t*)a.in + eb;
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      v[i] = valid ? load_coef(a, pc, eb, xmap<LOGN, FIRST>(lt, i), G::N) : 0u;
+      for (int i = 0; i < 32; ++i) {
+        const int x = xmap<LOGN, FIRST>(lt, i);
+        const bool ld = valid && x < a.len && !(upper_zero && i >= 16);
+        v[i] = ld ? __ldg(src + x) : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (upper_zero && i >= 16) {
+          v[i] = 0;
+          continue;
+        }
+        v[i] = valid ? load_coef(a, pc, eb, xmap<LOGN, FIRST>(lt, i), G::N) : 0u;
+      }
+    }
   } else {
     // small N: cooperative coalesced load of TPC transforms through smem
     for (int idx = tid; idx < G::TPC * G::N; idx += G::THREADS) {
@@ -169,26 +208,30 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   }
 
   if (G::NPASS == 1) {
-    dif_pass<LOGN, MAP_LAST>(v, lt, pc.tw, p);
-  } else if (G::NPASS == 2) {
-    dif_pass<LOGN, MAP_TOP>(v, lt, pc.tw, p);
-    __syncthreads();
-    to_smem<LOGN, MAP_TOP>(smt, v, lt);
-    __syncthreads();
-    from_smem<LOGN, MAP_LAST>(smt, v, lt);
-    dif_pass<LOGN, MAP_LAST>(v, lt, pc.tw, p);
+    dif_small<5>(v, pc.w32, p, false);
   } else {
-    dif_pass<LOGN, MAP_TOP>(v, lt, pc.tw, p);
+    {
+      Row r1;
+      row_load(r1, pc.tw + lt * 32);  // w^(lt * kappa)
+      dif_small<5>(v, pc.w32, p, upper_zero);
+      row_apply(v, r1, p);
+    }
     __syncthreads();
     to_smem<LOGN, MAP_TOP>(smt, v, lt);
-    __syncthreads();
-    from_smem<LOGN, MAP_MID>(smt, v, lt);
-    dif_pass<LOGN, MAP_MID>(v, lt, pc.tw, p);
-    __syncthreads();
-    to_smem<LOGN, MAP_MID>(smt, v, lt);
+    if (G::NPASS == 3) {
+      constexpr int lo = LOGN - 10;
+      Row r2;
+      row_load(r2, pc.tw + (lt & ((1 << lo) - 1)) * 32 * 32);  // w^(32 lt' kappa')
+      __syncthreads();
+      from_smem<LOGN, MAP_MID>(smt, v, lt);
+      dif_small<5>(v, pc.w32, p, false);
+      row_apply(v, r2, p);
+      __syncthreads();
+      to_smem<LOGN, MAP_MID>(smt, v, lt);
+    }
     __syncthreads();
     from_smem<LOGN, MAP_LAST>(smt, v, lt);
-    dif_pass<LOGN, MAP_LAST>(v, lt, pc.tw, p);
+    dif_small<G::LAST_R>(v, pc.w32, p, false);
   }
   if (!valid) return;
   uint32_t* out = a.out + (long long)blockIdx.z * a.out_prime_stride;
@@ -209,12 +252,12 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   }
 }
 
-template <int LOGN>
+template <int LOGN, bool SINGLE>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
-    ntt_inv_kernel(NttInvArgs a, PrimeSet ps) {
+    ntt_inv_kernel(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps) {
   using G = Geo<LOGN>;
   extern __shared__ uint32_t sm[];
-  const PrimeConst& pc = ps.pr[blockIdx.z];
+  const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
   const uint32_t p = pc.p;
   const int tid = threadIdx.x;
   const int tr = tid / G::TPT, lt = tid % G::TPT;
@@ -249,26 +292,37 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
 
   constexpr int FINAL = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
   if (G::NPASS == 1) {
-    dit_pass<LOGN, MAP_LAST>(v, lt, pc.itw, p);
-  } else if (G::NPASS == 2) {
-    dit_pass<LOGN, MAP_LAST>(v, lt, pc.itw, p);
-    __syncthreads();
-    to_smem<LOGN, MAP_LAST>(smt, v, lt);
-    __syncthreads();
-    from_smem<LOGN, MAP_TOP>(smt, v, lt);
-    dit_pass<LOGN, MAP_TOP>(v, lt, pc.itw, p);
+    dit_small<5>(v, pc.iw32, p);
   } else {
-    dit_pass<LOGN, MAP_LAST>(v, lt, pc.itw, p);
-    __syncthreads();
-    to_smem<LOGN, MAP_LAST>(smt, v, lt);
-    __syncthreads();
-    from_smem<LOGN, MAP_MID>(smt, v, lt);
-    dit_pass<LOGN, MAP_MID>(v, lt, pc.itw, p);
-    __syncthreads();
-    to_smem<LOGN, MAP_MID>(smt, v, lt);
-    __syncthreads();
-    from_smem<LOGN, MAP_TOP>(smt, v, lt);
-    dit_pass<LOGN, MAP_TOP>(v, lt, pc.itw, p);
+    if (G::NPASS == 3) {
+      constexpr int lo = LOGN - 10;
+      Row r2;
+      row_load(r2, pc.itw + (lt & ((1 << lo) - 1)) * 32 * 32);
+      dit_small<G::LAST_R>(v, pc.iw32, p);
+      __syncthreads();
+      to_smem<LOGN, MAP_LAST>(smt, v, lt);
+      __syncthreads();
+      from_smem<LOGN, MAP_MID>(smt, v, lt);
+      row_apply(v, r2, p);
+      Row r1;
+      row_load(r1, pc.itw + lt * 32);
+      dit_small<5>(v, pc.iw32, p);
+      __syncthreads();
+      to_smem<LOGN, MAP_MID>(smt, v, lt);
+      __syncthreads();
+      from_smem<LOGN, MAP_TOP>(smt, v, lt);
+      row_apply(v, r1, p);
+    } else {
+      Row r1;
+      row_load(r1, pc.itw + lt * 32);
+      dit_small<G::LAST_R>(v, pc.iw32, p);
+      __syncthreads();
+      to_smem<LOGN, MAP_LAST>(smt, v, lt);
+      __syncthreads();
+      from_smem<LOGN, MAP_TOP>(smt, v, lt);
+      row_apply(v, r1, p);
+    }
+    dit_small<5>(v, pc.iw32, p);
   }
   if (a.scale) {
 #pragma unroll
@@ -306,40 +360,50 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   }
 }
 
-template <int LOGN>
-int fwd_impl(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
+template <int LOGN, bool SINGLE>
+int fwd_launch(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
   using G = Geo<LOGN>;
   if (G::SMEM_BYTES > 48 * 1024) {
     static bool once = false;
     if (!once) {
-      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN>,
+      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, SINGLE>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         G::SMEM_BYTES));
       once = true;
     }
   }
   dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_fwd_kernel<LOGN><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  ntt_fwd_kernel<LOGN, SINGLE><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <int LOGN>
+int fwd_impl(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
+  return ps.count == 1 ? fwd_launch<LOGN, true>(a, ps, st) : fwd_launch<LOGN, false>(a, ps, st);
+}
+
+template <int LOGN, bool SINGLE>
+int inv_launch(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
+  using G = Geo<LOGN>;
+  if (G::SMEM_BYTES > 48 * 1024) {
+    static bool once = false;
+    if (!once) {
+      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, SINGLE>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        G::SMEM_BYTES));
+      once = true;
+    }
+  }
+  dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
+  ntt_inv_kernel<LOGN, SINGLE><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
   FPM_LAUNCH_CHECK();
   return kOk;
 }
 
 template <int LOGN>
 int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  using G = Geo<LOGN>;
-  if (G::SMEM_BYTES > 48 * 1024) {
-    static bool once = false;
-    if (!once) {
-      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        G::SMEM_BYTES));
-      once = true;
-    }
-  }
-  dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_inv_kernel<LOGN><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
-  FPM_LAUNCH_CHECK();
-  return kOk;
+  return ps.count == 1 ? inv_launch<LOGN, true>(a, ps, st) : inv_launch<LOGN, false>(a, ps, st);
 }
 
 }  // namespace

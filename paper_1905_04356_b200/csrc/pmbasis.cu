@@ -18,6 +18,12 @@
 #include "crt.cuh"
 
 namespace fpm {
+int mbasis_fast_max_order(int m, int n);
+int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long fs, int lf,
+                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev);
+}  // namespace fpm
+
+namespace fpm {
 
 namespace {
 
@@ -306,10 +312,15 @@ int leaf(Context& cx, uint64_t p, int is64, const void* F, int m, int n, long lo
   if (m > 0)
     FPM_CUDA_TRY(cudaMemcpyAsync(s_dev, s.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice,
                                  cx.stream()));
-  if (is64)
+  const bool fast = !is64 && p < (1ull << 31) && order >= 1 && order <= mbasis_fast_max_order(m, n);
+  if (fast) {
+    FPM_TRY(mbasis_fast(cx, (uint32_t)p, F, m, n, fs, lf, order, s_dev, P, ps, sft_dev));
+    FPM_TRY(launch_max_len(P, 0, (long long)m * m, (int)ps, lp_dev, cx.stream()));
+  } else if (is64) {
     FPM_TRY(launch_leaf<uint64_t>(cx, p, F, m, n, fs, lf, order, s_dev, P, ps, lp_dev, sft_dev));
-  else
+  } else {
     FPM_TRY(launch_leaf<uint32_t>(cx, p, F, m, n, fs, lf, order, s_dev, P, ps, lp_dev, sft_dev));
+  }
   FPM_CUDA_TRY(cudaMemcpyAsync(lp, lp_dev, sizeof(int), cudaMemcpyDeviceToHost, cx.stream()));
   if (sft_out) {
     sft_out->resize(m);
@@ -402,6 +413,12 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
                 int lf, int order, const int64_t* shift, int T, void* P, long long ps, int* lp,
                 int64_t* rdeg_out) {
   if (T < 1) T = 1;
+  // the output does not depend on T (product of canonical steps): cap it so
+  // leaves run on the shared-memory M-Basis kernels when they apply
+  if (!is64 && p < (1ull << 31)) {
+    const int tf = mbasis_fast_max_order(m, n);
+    if (tf >= 1 && T > tf) T = tf;
+  }
   std::vector<int64_t> s(shift, shift + m);
   FPM_TRY(pmbasis_rec(cx, p, is64, F, m, n, fs, lf, order, s, T, P, ps, lp));
   if (rdeg_out) {

@@ -170,25 +170,40 @@ int Context::plan(uint32_t p, int logn, const Plan** out) {
     set_last_error("p=%u supports transforms up to length 2^%d, not 2^%d", p, k, logn);
     return kOrderTooSmall;
   }
-  const size_t N = (size_t)1 << logn, H = N / 2;
+  const size_t N = (size_t)1 << logn;
   // omega = root^(2^(k - logn)) (modring.py:233)
   const uint64_t omega = h_powmod(h_ntt_root(p), (uint64_t)1 << (k - logn), p);
   const uint64_t iomega = h_invmod(omega, p);
-  std::vector<uint2> tw(H), itw(H);
-  uint64_t w = 1, iw = 1;
-  for (size_t e = 0; e < H; ++e) {
-    tw[e] = make_uint2((uint32_t)w, h_shoup((uint32_t)w, p));
-    itw[e] = make_uint2((uint32_t)iw, h_shoup((uint32_t)iw, p));
-    w = h_mulmod(w, omega, p);
-    iw = h_mulmod(iw, iomega, p);
+  // twiddle rows: tw[r*32 + c] = omega^(r*c), r < N/32, c < 32 (4-step
+  // inter-pass twiddles; ntt.cu), same for omega^-1
+  std::vector<uint2> tw(N), itw(N);
+  const size_t rows = N / 32;
+  for (size_t r = 0; r < rows; ++r) {
+    const uint64_t wr = h_powmod(omega, r, p), iwr = h_powmod(iomega, r, p);
+    uint64_t w = 1, iw = 1;
+    for (size_t c = 0; c < 32; ++c) {
+      tw[r * 32 + c] = make_uint2((uint32_t)w, h_shoup((uint32_t)w, p));
+      itw[r * 32 + c] = make_uint2((uint32_t)iw, h_shoup((uint32_t)iw, p));
+      w = h_mulmod(w, wr, p);
+      iw = h_mulmod(iw, iwr, p);
+    }
   }
   Plan pl;
   pl.p = p;
   pl.logn = logn;
-  FPM_CUDA_TRY(cudaMalloc(&pl.tw, H * sizeof(uint2)));
-  FPM_CUDA_TRY(cudaMalloc(&pl.itw, H * sizeof(uint2)));
-  FPM_CUDA_TRY(cudaMemcpy(pl.tw, tw.data(), H * sizeof(uint2), cudaMemcpyHostToDevice));
-  FPM_CUDA_TRY(cudaMemcpy(pl.itw, itw.data(), H * sizeof(uint2), cudaMemcpyHostToDevice));
+  FPM_CUDA_TRY(cudaMalloc(&pl.tw, N * sizeof(uint2)));
+  FPM_CUDA_TRY(cudaMalloc(&pl.itw, N * sizeof(uint2)));
+  FPM_CUDA_TRY(cudaMemcpy(pl.tw, tw.data(), N * sizeof(uint2), cudaMemcpyHostToDevice));
+  FPM_CUDA_TRY(cudaMemcpy(pl.itw, itw.data(), N * sizeof(uint2), cudaMemcpyHostToDevice));
+  // radix-32 inner roots w32 = omega^(N/32) (logn >= 5 in every kernel)
+  const uint64_t w32 = h_powmod(omega, N >= 32 ? N / 32 : 1, p), iw32 = h_invmod(w32, p);
+  uint64_t a = 1, b = 1;
+  for (int e = 0; e < 16; ++e) {
+    pl.w32[e] = make_uint2((uint32_t)a, h_shoup((uint32_t)a, p));
+    pl.iw32[e] = make_uint2((uint32_t)b, h_shoup((uint32_t)b, p));
+    a = h_mulmod(a, w32, p);
+    b = h_mulmod(b, iw32, p);
+  }
   pl.ninv = (uint32_t)h_invmod(N % p, p);
   pl.ninv_sh = h_shoup(pl.ninv, p);
   auto res = plans_.emplace(key, pl);
@@ -251,6 +266,10 @@ int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   out->ninv_sh = pl->ninv_sh;
   out->tw = pl->tw;
   out->itw = pl->itw;
+  for (int e = 0; e < 16; ++e) {
+    out->w32[e] = pl->w32[e];
+    out->iw32[e] = pl->iw32[e];
+  }
   return kOk;
 }
 

@@ -12,9 +12,10 @@ namespace fpm {
 struct Plan {
   uint32_t p = 0;
   int logn = 0;
-  uint2* tw = nullptr;   // device, N/2 entries
-  uint2* itw = nullptr;  // device, N/2 entries
+  uint2* tw = nullptr;   // device, N entries (twiddle rows, see ntt.cu)
+  uint2* itw = nullptr;  // device, N entries
   uint32_t ninv = 0, ninv_sh = 0;
+  uint2 w32[16], iw32[16];
 };
 
 class Context {
