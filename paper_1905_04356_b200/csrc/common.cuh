@@ -123,6 +123,7 @@ struct PrimeConst {
   const uint2* itw;  // inverse rows: w^-(r*k), N entries
   uint2 w32[16];     // (w32^e, Shoup) e < 16, w32 = w^(N/32): inner radix-32 DFTs
   uint2 iw32[16];    // inverse roots
+  uint2 sc[4];       // (2^(8q) mod p, Shoup), q = 0..3: limb scaling (tc_pointwise.cu)
 };
 
 constexpr int kMaxPrimes = 8;

@@ -15,11 +15,13 @@
 namespace fpm {
 namespace {
 
-template <int LOGN>
+// PM (point-major output) launches use TPCX >= 4 transforms per CTA so each
+// evaluation point receives a >= 16-byte contiguous row segment.
+template <int LOGN, int TPCX = 0>
 struct Geo {
   static constexpr int N = 1 << LOGN;
   static constexpr int TPT = N / 32;                       // threads per transform
-  static constexpr int TPC = N >= 8192 ? 1 : 8192 / N;     // transforms per CTA
+  static constexpr int TPC = TPCX ? TPCX : (N >= 8192 ? 1 : 8192 / N);  // transforms per CTA
   static constexpr int THREADS = TPT * TPC;                // 256 (N<=8192), 512, 1024
   static constexpr int NPASS = (LOGN + 4) / 5;             // 1, 2 or 3 passes
   static constexpr int LAST_R = LOGN - 5 * (NPASS - 1);    // bits of the last pass
@@ -154,10 +156,10 @@ __device__ __forceinline__ uint32_t load_coef(const NttFwdArgs& a, const PrimeCo
 
 // SINGLE: one prime -> every PrimeConst field is a constant-bank operand
 // (no LDC); otherwise blockIdx.z selects the prime of a multi-prime batch.
-template <int LOGN, bool SINGLE>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS)
+template <int LOGN, bool SINGLE, int TPCX>
+__global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     ntt_fwd_kernel(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, TPCX>;
   extern __shared__ uint32_t sm[];
   const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
   const uint32_t p = pc.p;
@@ -233,8 +235,33 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
     from_smem<LOGN, MAP_LAST>(smt, v, lt);
     dif_small<G::LAST_R>(v, pc.w32, p, false);
   }
-  if (!valid) return;
   uint32_t* out = a.out + (long long)blockIdx.z * a.out_prime_stride;
+  if (a.pm) {
+    // point-major: out[x * n_entries + e], a CTA writes TPC consecutive
+    // entries of every point as 16-byte pieces (staged through smem)
+    __syncthreads();
+    to_smem<LOGN, MAP_LAST>(smt, v, lt);
+    __syncthreads();
+    constexpr int GQ = G::TPC / 4;
+    const bool vec = (a.n_entries & 3) == 0;
+    for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
+      const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
+      const long long eb = e0 + 4 * gq;
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) w[q] = sm[(4 * gq + q) * G::STRIDE + pad(x)];
+      uint32_t* dst = out + (long long)x * a.n_entries + eb;
+      if (vec && eb + 3 < a.n_entries) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (eb + q < a.n_entries) dst[q] = w[q];
+      }
+    }
+    return;
+  }
+  if (!valid) return;
   if (a.natural) {
     // public ntt_forward order: out[k] = F(w^k), k = bitrev(x)
 #pragma unroll
@@ -252,10 +279,10 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   }
 }
 
-template <int LOGN, bool SINGLE>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS)
+template <int LOGN, bool SINGLE, int TPCX>
+__global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     ntt_inv_kernel(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, TPCX>;
   extern __shared__ uint32_t sm[];
   const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
   const uint32_t p = pc.p;
@@ -275,6 +302,26 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
       const long long e2 = e0 + t2;
       const int x = __brev(k) >> (32 - LOGN);
       sm[t2 * G::STRIDE + pad(x)] = e2 < a.n_entries ? in[e2 * G::N + k] : 0u;
+    }
+    __syncthreads();
+    from_smem<LOGN, MAP_LAST>(smt, v, lt);
+  } else if (a.pm) {
+    constexpr int GQ = G::TPC / 4;
+    const bool vec = (a.n_entries & 3) == 0;
+    for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
+      const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
+      const long long eb = e0 + 4 * gq;
+      const uint32_t* src = in + (long long)x * a.n_entries + eb;
+      uint32_t w[4];
+      if (vec && eb + 3 < a.n_entries) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
+        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = eb + q < a.n_entries ? src[q] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sm[(4 * gq + q) * G::STRIDE + pad(x)] = w[q];
     }
     __syncthreads();
     from_smem<LOGN, MAP_LAST>(smt, v, lt);
@@ -360,50 +407,74 @@ __global__ void __launch_bounds__(Geo<LOGN>::THREADS)
   }
 }
 
-template <int LOGN, bool SINGLE>
+template <int LOGN, bool SINGLE, int TPCX>
 int fwd_launch(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, TPCX>;
   if (G::SMEM_BYTES > 48 * 1024) {
     static bool once = false;
     if (!once) {
-      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, SINGLE>,
+      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, SINGLE, TPCX>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         G::SMEM_BYTES));
       once = true;
     }
   }
   dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_fwd_kernel<LOGN, SINGLE><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  ntt_fwd_kernel<LOGN, SINGLE, TPCX><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
   FPM_LAUNCH_CHECK();
   return kOk;
 }
 
+// point-major launches: >= 4 (up to 8) transforms per CTA, <= 1024 threads
 template <int LOGN>
-int fwd_impl(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  return ps.count == 1 ? fwd_launch<LOGN, true>(a, ps, st) : fwd_launch<LOGN, false>(a, ps, st);
+constexpr int pm_tpc() {
+  return (1 << LOGN) <= 1024 ? 0 : ((1 << LOGN) <= 4096 ? 8 : (1 << (15 - LOGN)));
 }
 
-template <int LOGN, bool SINGLE>
+template <int LOGN>
+int fwd_impl(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
+  if (a.pm) {
+    if constexpr (pm_tpc<LOGN>() >= 4 || pm_tpc<LOGN>() == 0) {
+      return ps.count == 1 ? fwd_launch<LOGN, true, pm_tpc<LOGN>()>(a, ps, st)
+                           : fwd_launch<LOGN, false, pm_tpc<LOGN>()>(a, ps, st);
+    } else {
+      set_last_error("point-major NTT layout needs N <= 2^13");
+      return kUnsupported;
+    }
+  }
+  return ps.count == 1 ? fwd_launch<LOGN, true, 0>(a, ps, st) : fwd_launch<LOGN, false, 0>(a, ps, st);
+}
+
+template <int LOGN, bool SINGLE, int TPCX>
 int inv_launch(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  using G = Geo<LOGN>;
+  using G = Geo<LOGN, TPCX>;
   if (G::SMEM_BYTES > 48 * 1024) {
     static bool once = false;
     if (!once) {
-      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, SINGLE>,
+      FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, SINGLE, TPCX>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         G::SMEM_BYTES));
       once = true;
     }
   }
   dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_inv_kernel<LOGN, SINGLE><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  ntt_inv_kernel<LOGN, SINGLE, TPCX><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
   FPM_LAUNCH_CHECK();
   return kOk;
 }
 
 template <int LOGN>
 int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  return ps.count == 1 ? inv_launch<LOGN, true>(a, ps, st) : inv_launch<LOGN, false>(a, ps, st);
+  if (a.pm) {
+    if constexpr (pm_tpc<LOGN>() >= 4 || pm_tpc<LOGN>() == 0) {
+      return ps.count == 1 ? inv_launch<LOGN, true, pm_tpc<LOGN>()>(a, ps, st)
+                           : inv_launch<LOGN, false, pm_tpc<LOGN>()>(a, ps, st);
+    } else {
+      set_last_error("point-major NTT layout needs N <= 2^13");
+      return kUnsupported;
+    }
+  }
+  return ps.count == 1 ? inv_launch<LOGN, true, 0>(a, ps, st) : inv_launch<LOGN, false, 0>(a, ps, st);
 }
 
 }  // namespace

@@ -34,8 +34,9 @@ struct NttFwdArgs {
   int fold;                  // len > N: fold cyclically mod x^N - 1
   int reduce;                // inputs may be >= p: reduce on load
   int natural;               // 1: natural-order output out[e*N + k] (public API)
+  int pm;                    // 1: point-major output out[x*n_entries + e]
   int n_entries;
-  uint32_t* out;             // eval layout E[N/32][n_entries][32] (or natural)
+  uint32_t* out;             // eval layout E[N/32][n_entries][32] (or natural / PM)
   long long out_prime_stride;
 };
 
@@ -43,6 +44,7 @@ struct NttInvArgs {
   const uint32_t* in;        // eval layout (or natural when natural != 0)
   long long in_prime_stride;
   int natural;               // 1: natural-order input in[e*N + k] (public API)
+  int pm;                    // 1: point-major input in[x*n_entries + e]
   int n_entries;
   uint32_t* out;             // out[e * out_stride + t] = coeff[(off + t) mod N]
   long long out_stride;

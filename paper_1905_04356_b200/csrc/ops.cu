@@ -4,6 +4,8 @@
 #include "crt.cuh"
 #include "ntt.cuh"
 #include "pointwise.cuh"
+#include "tc_pointwise.cuh"
+#include <cstdlib>
 
 namespace fpm {
 
@@ -143,11 +145,15 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   FPM_TRY(ws.get(r * N * ec, &EC));
 
   const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
+  // large contractions: int8 tensor-core pointwise on point-major operands
+  static const bool tc_off = std::getenv("FPM_DISABLE_TC") != nullptr;
+  bool use_tc = !tc_off && logn <= 13;
+  for (int i = 0; i < r && use_tc; ++i) use_tc = tc_pointwise_applicable(m, k, n, primes[i]);
   // forward transforms (all primes in one launch: blockIdx.z = prime)
   NttFwdArgs fa{};
   fa.in = A.ptr; fa.in64 = A.is64; fa.in_stride = A.stride; fa.in_prime_stride = 0;
   fa.len = A.len; fa.fold = 0; fa.reduce = reduce_needed || (!direct && A.is64);
-  fa.natural = 0; fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
+  fa.natural = 0; fa.pm = use_tc; fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
   if (direct && A.is64) fa.reduce = 0;
   {
     StageTimer t_(cx, "ntt_fwd_A");
@@ -163,16 +169,22 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
   }
 
-  PointwiseArgs pa{};
-  pa.A = EA; pa.B = EB; pa.C = EC; pa.m = m; pa.k = k; pa.n = n; pa.nblk = (int)(N / 32);
-  pa.a_prime_stride = N * ea; pa.b_prime_stride = N * eb; pa.c_prime_stride = N * ec;
-  {
+  if (use_tc) {
+    TcArgs ta{};
+    ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
+    ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
+    StageTimer t_(cx, "pointwise_tc");
+    FPM_TRY(launch_tc_pointwise(ta, ps, st));
+  } else {
+    PointwiseArgs pa{};
+    pa.A = EA; pa.B = EB; pa.C = EC; pa.m = m; pa.k = k; pa.n = n; pa.nblk = (int)(N / 32);
+    pa.a_prime_stride = N * ea; pa.b_prime_stride = N * eb; pa.c_prime_stride = N * ec;
     StageTimer t_(cx, "pointwise");
     FPM_TRY(launch_pointwise(pa, ps, st));
   }
 
   NttInvArgs ia{};
-  ia.in = EC; ia.in_prime_stride = N * ec; ia.natural = 0; ia.n_entries = (int)ec;
+  ia.in = EC; ia.in_prime_stride = N * ec; ia.natural = 0; ia.pm = use_tc; ia.n_entries = (int)ec;
   ia.out_len = wlen; ia.off = (int)off; ia.scale = 1;
   if (direct && !C.is64) {
     ia.out = (uint32_t*)C.ptr; ia.out_stride = C.stride; ia.out_prime_stride = 0;

@@ -264,6 +264,10 @@ int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   out->mu = (uint64_t)((((u128)1) << 64) / p);
   out->ninv = pl->ninv;
   out->ninv_sh = pl->ninv_sh;
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t v = (uint32_t)(((uint64_t)1 << (8 * q)) % p);
+    out->sc[q] = make_uint2(v, h_shoup(v, p));
+  }
   out->tw = pl->tw;
   out->itw = pl->itw;
   for (int e = 0; e < 16; ++e) {

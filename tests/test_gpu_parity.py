@@ -106,6 +106,12 @@ def _dense_rand(p, shape, seed):
     (1152921493869428737, 3, 3, 3, 200, 200),
     (786433, 6, 6, 6, 2000, 2000),
     (97, 4, 4, 4, 500, 500),
+    # tensor-core pointwise path (m >= 64, k >= 64, n >= 32), incl. ragged shapes
+    (P31, 72, 128, 40, 300, 200),
+    (P31, 64, 64, 64, 1000, 1000),
+    (P31, 130, 68, 33, 40, 90),
+    (P60, 64, 64, 64, 100, 100),
+    (1152921493869428737, 64, 96, 32, 64, 64),
 ])
 def test_pm_mul_vs_oracle(p, m, k, n, la, lb):
     A = _dense_rand(p, (m, k, la), 10 + m)
