@@ -58,6 +58,12 @@ struct NttInvArgs {
 int launch_ntt_fwd(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
 int launch_ntt_inv(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// persistent kernels (ntt_persist.cu) for the common cases, N <= 8192
+bool ntt_persist_fwd_ok(int logn, const NttFwdArgs& a);
+bool ntt_persist_inv_ok(int logn, const NttInvArgs& a);
+int launch_ntt_fwd_persist(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
+int launch_ntt_inv_persist(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 constexpr int kMinLogN = 5;
 constexpr int kMaxLogN = 15;
 

@@ -1,0 +1,405 @@
+// ntt_persist.cu -- persistent batched NTT kernels (N <= 8192, 31-bit primes).
+//
+// Same four-step radix-32 network as ntt.cu, organised for latency hiding:
+//   * each CTA stays resident and loops over groups of TPC transforms;
+//   * the (row, kappa) twiddle table is staged ONCE per CTA in shared memory
+//     (XOR-swizzled by row so 16-byte row reads are bank-conflict free) --
+//     no global twiddle loads inside the passes;
+//   * the next group's input is prefetched into 32 registers per thread
+//     while the current group runs its passes, so HBM latency overlaps
+//     butterfly work instead of stalling it.
+// Forward: u32 input (no fold / no reduction), blocked-eval or point-major
+// output.  Inverse: blocked-eval or point-major input.
+#include "ntt.cuh"
+#include "ntt_passes.cuh"
+
+namespace fpm {
+namespace {
+using namespace nttp;
+
+// pair q (entries 2q, 2q+1) of twiddle row r is stored at pair q ^ sw(r)
+__device__ __forceinline__ int sw_row(int r) { return (r ^ (r >> 5)) & 7; }
+
+// v[i] *= row r [brev5(i)], pairs read from the swizzled smem table just in time
+__device__ __forceinline__ void row_apply_s(uint32_t (&v)[32], const uint2* tws, int r,
+                                            uint32_t p) {
+  const uint4* base = reinterpret_cast<const uint4*>(tws + (size_t)r * 32);
+  const int s = sw_row(r);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const uint4 t = base[q ^ s];
+    const int k0 = 2 * q, k1 = 2 * q + 1;
+    if (k0) {
+      const int i0 = brev5(k0);
+      v[i0] = d_red(d_shoup(v[i0], t.x, t.y, p), p);
+    }
+    const int i1 = brev5(k1);
+    v[i1] = d_red(d_shoup(v[i1], t.z, t.w, p), p);
+  }
+}
+
+template <int LOGN>
+__device__ __forceinline__ void stage_table(uint2* tws, const uint2* __restrict__ tw) {
+  constexpr int N = 1 << LOGN;
+  // N entries = N/32 rows x 16 pairs
+  for (int idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
+    const int r = idx >> 4, q = idx & 15;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(tw) + idx);
+    reinterpret_cast<uint4*>(tws)[r * 16 + (q ^ sw_row(r))] = v;
+  }
+}
+
+template <int LOGN, int TPCX>
+__device__ __forceinline__ void fwd_passes(uint32_t (&v)[32], uint32_t* smt, const uint2* tws,
+                                           const PrimeConst& pc, int lt, bool upper_zero) {
+  using G = Geo<LOGN, TPCX>;
+  const uint32_t p = pc.p;
+  if (G::NPASS == 1) {
+    dif_small<5>(v, pc.w32, p, false);
+    return;
+  }
+  dif_small<5>(v, pc.w32, p, upper_zero);
+  row_apply_s(v, tws, lt, p);
+  __syncthreads();
+  to_smem<LOGN, MAP_TOP>(smt, v, lt);
+  if (G::NPASS == 3) {
+    constexpr int lo = LOGN - 10;
+    __syncthreads();
+    from_smem<LOGN, MAP_MID>(smt, v, lt);
+    dif_small<5>(v, pc.w32, p, false);
+    row_apply_s(v, tws, (lt & ((1 << lo) - 1)) * 32, p);
+    __syncthreads();
+    to_smem<LOGN, MAP_MID>(smt, v, lt);
+  }
+  __syncthreads();
+  from_smem<LOGN, MAP_LAST>(smt, v, lt);
+  dif_small<G::LAST_R>(v, pc.w32, p, false);
+}
+
+template <int LOGN, int TPCX>
+__device__ __forceinline__ void inv_passes(uint32_t (&v)[32], uint32_t* smt, const uint2* tws,
+                                           const PrimeConst& pc, int lt) {
+  using G = Geo<LOGN, TPCX>;
+  const uint32_t p = pc.p;
+  if (G::NPASS == 1) {
+    dit_small<5>(v, pc.iw32, p);
+    return;
+  }
+  dit_small<G::LAST_R>(v, pc.iw32, p);
+  __syncthreads();
+  to_smem<LOGN, MAP_LAST>(smt, v, lt);
+  __syncthreads();
+  if (G::NPASS == 3) {
+    constexpr int lo = LOGN - 10;
+    from_smem<LOGN, MAP_MID>(smt, v, lt);
+    row_apply_s(v, tws, (lt & ((1 << lo) - 1)) * 32, p);
+    dit_small<5>(v, pc.iw32, p);
+    __syncthreads();
+    to_smem<LOGN, MAP_MID>(smt, v, lt);
+    __syncthreads();
+  }
+  from_smem<LOGN, MAP_TOP>(smt, v, lt);
+  row_apply_s(v, tws, lt, p);
+  dit_small<5>(v, pc.iw32, p);
+}
+
+template <int THREADS>
+constexpr int min_blocks() {
+  return THREADS <= 256 ? 2 : 1;  // <= 128 registers per thread
+}
+
+template <int LOGN, bool SINGLE, int TPCX>
+__global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN, TPCX>::THREADS>())
+    ntt_fwd_persist(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps) {
+  using G = Geo<LOGN, TPCX>;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
+  const int z = SINGLE ? 0 : blockIdx.z;
+  const PrimeConst& pc = ps.pr[z];
+  const int tid = threadIdx.x;
+  const int tr = tid / G::TPT, lt = tid % G::TPT;
+  uint32_t* smt = sm + tr * G::STRIDE;
+  const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
+  const uint32_t* in = (const uint32_t*)a.in + (long long)z * a.in_prime_stride;
+  uint32_t* out = a.out + (long long)z * a.out_prime_stride;
+  const bool upper_zero = G::NPASS > 1 && a.len <= G::N / 2;
+  constexpr int FIRST = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
+
+  stage_table<LOGN>(tws, pc.tw);
+
+  uint32_t pre[32];
+  auto load_group = [&](long long grp) {
+    if (G::TPT >= 32) {
+      const long long e = grp * G::TPC + tr;
+      const bool valid = e < a.n_entries;
+      const uint32_t* src = in + e * a.in_stride;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int x = xmap<LOGN, FIRST>(lt, i);
+        pre[i] = (valid && x < a.len && !(upper_zero && i >= 16)) ? __ldg(src + x) : 0u;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int idx = tid + u * G::THREADS;
+        const int t2 = idx >> LOGN, x = idx & (G::N - 1);
+        const long long e = grp * G::TPC + t2;
+        pre[u] = (e < a.n_entries && x < a.len) ? __ldg(in + e * a.in_stride + x) : 0u;
+      }
+    }
+  };
+
+  long long grp = blockIdx.x;
+  if (grp < groups) load_group(grp);
+  __syncthreads();  // table staged
+  for (; grp < groups; grp += gridDim.x) {
+    uint32_t v[32];
+    if (G::TPT >= 32) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = pre[i];
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const int idx = tid + u * G::THREADS;
+        sm[(idx >> LOGN) * G::STRIDE + pad(idx & (G::N - 1))] = pre[u];
+      }
+      __syncthreads();
+      from_smem<LOGN, FIRST>(smt, v, lt);
+    }
+    const long long nxt = grp + gridDim.x;
+    constexpr bool kPrefetch = G::THREADS <= 512;  // 32 extra registers
+    if (kPrefetch && nxt < groups) load_group(nxt);  // in flight during the passes
+    fwd_passes<LOGN, TPCX>(v, smt, tws, pc, lt, upper_zero);
+    const long long e0 = grp * G::TPC, e = e0 + tr;
+    if (a.pm) {
+      __syncthreads();
+      to_smem<LOGN, MAP_LAST>(smt, v, lt);
+      __syncthreads();
+      constexpr int GQ = G::TPC / 4;
+      const bool vec = (a.n_entries & 3) == 0;
+      for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
+        const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
+        const long long eb = e0 + 4 * gq;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = sm[(4 * gq + q) * G::STRIDE + pad(x)];
+        uint32_t* dst = out + (long long)x * a.n_entries + eb;
+        if (vec && eb + 3 < a.n_entries) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (eb + q < a.n_entries) dst[q] = w[q];
+        }
+      }
+    } else if (e < a.n_entries) {
+      uint4* dst = reinterpret_cast<uint4*>(out + ((long long)lt * a.n_entries + e) * 32);
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
+    __syncthreads();  // smem exchange buffer reused by the next group
+    if (!kPrefetch && nxt < groups) load_group(nxt);
+  }
+}
+
+template <int LOGN, bool SINGLE, int TPCX>
+__global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN, TPCX>::THREADS>())
+    ntt_inv_persist(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps) {
+  using G = Geo<LOGN, TPCX>;
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
+  const int z = SINGLE ? 0 : blockIdx.z;
+  const PrimeConst& pc = ps.pr[z];
+  const uint32_t p = pc.p;
+  const int tid = threadIdx.x;
+  const int tr = tid / G::TPT, lt = tid % G::TPT;
+  uint32_t* smt = sm + tr * G::STRIDE;
+  const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
+  const uint32_t* in = a.in + (long long)z * a.in_prime_stride;
+  uint32_t* out = a.out + (long long)z * a.out_prime_stride;
+  constexpr int FINAL = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
+  constexpr int GQ = G::TPC / 4;
+
+  stage_table<LOGN>(tws, pc.itw);
+
+  uint32_t pre[32];
+  auto load_group = [&](long long grp) {
+    const long long e0 = grp * G::TPC;
+    if (a.pm) {
+      // this thread's share of the group's point-major input: 16-byte pieces
+      const bool vec = (a.n_entries & 3) == 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = tid + u * G::THREADS;
+        const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
+        const long long eb = e0 + 4 * gq;
+        const uint32_t* src = in + (long long)x * a.n_entries + eb;
+        if (vec && eb + 3 < a.n_entries) {
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
+          pre[4 * u] = t.x; pre[4 * u + 1] = t.y; pre[4 * u + 2] = t.z; pre[4 * u + 3] = t.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) pre[4 * u + q] = eb + q < a.n_entries ? src[q] : 0u;
+        }
+      }
+    } else {
+      const long long e = e0 + tr;
+      if (e < a.n_entries) {
+        const uint4* src = reinterpret_cast<const uint4*>(in + ((long long)lt * a.n_entries + e) * 32);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 t = __ldg(src + q);
+          pre[4 * q] = t.x; pre[4 * q + 1] = t.y; pre[4 * q + 2] = t.z; pre[4 * q + 3] = t.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pre[i] = 0;
+      }
+    }
+  };
+
+  long long grp = blockIdx.x;
+  if (grp < groups) load_group(grp);
+  __syncthreads();
+  for (; grp < groups; grp += gridDim.x) {
+    uint32_t v[32];
+    if (a.pm) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = tid + u * G::THREADS;
+        const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sm[(4 * gq + q) * G::STRIDE + pad(x)] = pre[4 * u + q];
+      }
+      __syncthreads();
+      from_smem<LOGN, MAP_LAST>(smt, v, lt);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = pre[i];
+    }
+    const long long nxt = grp + gridDim.x;
+    constexpr bool kPrefetch = G::THREADS <= 512;
+    if (kPrefetch && nxt < groups) load_group(nxt);
+    inv_passes<LOGN, TPCX>(v, smt, tws, pc, lt);
+    if (a.scale) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = d_red(d_shoup(v[i], pc.ninv, pc.ninv_sh, p), p);
+    }
+    const long long e0 = grp * G::TPC, e = e0 + tr;
+    if (G::TPT >= 32) {
+      if (e < a.n_entries) {
+        uint32_t* oe = out + e * a.out_stride;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int t = (xmap<LOGN, FINAL>(lt, i) - a.off) & (G::N - 1);
+          if (t < a.out_len) oe[t] = v[i];
+        }
+      }
+    } else {
+      __syncthreads();
+      to_smem<LOGN, FINAL>(smt, v, lt);
+      __syncthreads();
+      const int ol = a.out_len < G::N ? a.out_len : G::N;
+      for (int idx = tid; idx < G::TPC * ol; idx += G::THREADS) {
+        const int t2 = idx / ol, t = idx - t2 * ol;
+        const long long e2 = e0 + t2;
+        if (e2 < a.n_entries) {
+          const int x = (t + a.off) & (G::N - 1);
+          out[e2 * a.out_stride + t] = sm[t2 * G::STRIDE + pad(x)];
+        }
+      }
+    }
+    __syncthreads();
+    if (!kPrefetch && nxt < groups) load_group(nxt);
+  }
+}
+
+// point-major: 4 transforms per CTA (16-byte row pieces), <= 512 threads for N <= 4096
+template <int LOGN>
+constexpr int pm_tpc2() {
+  return (1 << LOGN) <= 2048 ? 0 : 4;
+}
+
+template <int LOGN, bool SINGLE, int TPCX, bool FWD, typename Args>
+int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
+  using G = Geo<LOGN, TPCX>;
+  const size_t smem = (size_t)((G::TPC * G::STRIDE + 3) & ~3) * 4 + (size_t)G::N * 8;
+  const void* kern;
+  if constexpr (FWD)
+    kern = (const void*)ntt_fwd_persist<LOGN, SINGLE, TPCX>;
+  else
+    kern = (const void*)ntt_inv_persist<LOGN, SINGLE, TPCX>;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    FPM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+    FPM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern,
+                                                               G::THREADS, smem));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
+  long long grid = (long long)blocks_per_sm * sms / ps.count;
+  if (grid < 1) grid = 1;
+  if (grid > groups) grid = groups;
+  dim3 g3((unsigned)grid, 1, (unsigned)ps.count);
+  if constexpr (FWD)
+    ntt_fwd_persist<LOGN, SINGLE, TPCX><<<g3, G::THREADS, smem, st>>>(a, ps);
+  else
+    ntt_inv_persist<LOGN, SINGLE, TPCX><<<g3, G::THREADS, smem, st>>>(a, ps);
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+template <int LOGN, bool FWD, typename Args>
+int persist_impl(const Args& a, const PrimeSet& ps, cudaStream_t st) {
+  if (a.pm) {
+    return ps.count == 1 ? persist_launch<LOGN, true, pm_tpc2<LOGN>(), FWD>(a, ps, st)
+                         : persist_launch<LOGN, false, pm_tpc2<LOGN>(), FWD>(a, ps, st);
+  }
+  return ps.count == 1 ? persist_launch<LOGN, true, 0, FWD>(a, ps, st)
+                       : persist_launch<LOGN, false, 0, FWD>(a, ps, st);
+}
+
+}  // namespace
+
+bool ntt_persist_fwd_ok(int logn, const NttFwdArgs& a) {
+  return logn >= 5 && logn <= 13 && !a.fold && !a.in64 && !a.reduce && !a.natural;
+}
+bool ntt_persist_inv_ok(int logn, const NttInvArgs& a) {
+  return logn >= 5 && logn <= 13 && !a.natural;
+}
+
+int launch_ntt_fwd_persist(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
+  switch (logn) {
+    case 5: return persist_impl<5, true>(a, ps, st);
+    case 6: return persist_impl<6, true>(a, ps, st);
+    case 7: return persist_impl<7, true>(a, ps, st);
+    case 8: return persist_impl<8, true>(a, ps, st);
+    case 9: return persist_impl<9, true>(a, ps, st);
+    case 10: return persist_impl<10, true>(a, ps, st);
+    case 11: return persist_impl<11, true>(a, ps, st);
+    case 12: return persist_impl<12, true>(a, ps, st);
+    case 13: return persist_impl<13, true>(a, ps, st);
+  }
+  return kUnsupported;
+}
+
+int launch_ntt_inv_persist(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
+  switch (logn) {
+    case 5: return persist_impl<5, false>(a, ps, st);
+    case 6: return persist_impl<6, false>(a, ps, st);
+    case 7: return persist_impl<7, false>(a, ps, st);
+    case 8: return persist_impl<8, false>(a, ps, st);
+    case 9: return persist_impl<9, false>(a, ps, st);
+    case 10: return persist_impl<10, false>(a, ps, st);
+    case 11: return persist_impl<11, false>(a, ps, st);
+    case 12: return persist_impl<12, false>(a, ps, st);
+    case 13: return persist_impl<13, false>(a, ps, st);
+  }
+  return kUnsupported;
+}
+
+}  // namespace fpm

@@ -38,7 +38,8 @@ constexpr uint32_t TILE_A = (MG / 8) * SBO_A;        // 32768
 constexpr uint32_t TILE_B = (4 * NB / 8) * SBO_B;    // 33280
 constexpr uint32_t STAGE = TILE_A + TILE_B;
 constexpr int NSTAGE = 3;
-constexpr size_t kSmem = (size_t)NSTAGE * STAGE + 1024;
+constexpr uint32_t B32 = KL * NB * 4;               // raw u32 B block (8 KB)
+constexpr size_t kSmem = (size_t)NSTAGE * STAGE + 2 * B32 + 1024;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool ok) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src),
@@ -79,13 +80,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t* Bt = a.B + z * a.b_ps + t * (long long)k * n;
     const int i0 = mg * MG, j0 = jb * NB;
 
-    for (int ch = 0; ch < nch; ++ch, ++g) {
-      const int s = (int)(g % NSTAGE);
-      if (g >= NSTAGE) tc::mbar_wait(&mbar[s], (uint32_t)(((g / NSTAGE) - 1) & 1));
-      const uint32_t tA = sbase + s * STAGE, tB = tA + TILE_A;
-      uint8_t* pB = smem + s * STAGE + TILE_A;
+    // Pipeline per chunk g: loads of chunk g+1 (raw A bytes straight into its
+    // UMMA tile, the u32 B block into a staging buffer) are in flight while
+    // chunk g's B tile is built from smem and while the tensor core runs
+    // chunk g-1.
+    auto issue_loads = [&](int ch, long long gg) {
+      const int s = (int)(gg % NSTAGE);
+      const uint32_t tA = sbase + s * STAGE;
+      const uint32_t tS = sbase + NSTAGE * STAGE + (uint32_t)(gg & 1) * B32;
       const int l0 = ch * KL;
-      // ---- A tile: raw bytes of A[i][l0 .. l0+32) (K' = 4l + q) -------------
 #pragma unroll
       for (int u = 0; u < (MG * 8) / kThreads; ++u) {
         const int q = tid + u * kThreads;
@@ -95,16 +98,54 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t* src = At + (ok ? (long long)gi * k + gl : 0);
         cp_async16(tA + (r >> 3) * SBO_A + kc * 128 + (r & 7) * 16, src, ok);
       }
+      // B block rows l0..l0+31, columns j0..j0+63 (16-byte pieces when aligned)
+      if ((n & 3) == 0) {
+#pragma unroll
+        for (int u = 0; u < (KL * NB / 4) / kThreads; ++u) {
+          const int q = tid + u * kThreads;
+          const int ll = q >> 4, jq = q & 15;
+          const int gl = l0 + ll, gj = j0 + 4 * jq;
+          const bool ok = gl < k && gj < n;
+          const uint32_t* src = Bt + (ok ? (long long)gl * n + gj : 0);
+          cp_async16(tS + (ll * NB + 4 * jq) * 4, src, ok);
+        }
+      } else {
+        uint32_t* dS = reinterpret_cast<uint32_t*>(smem + NSTAGE * STAGE + (gg & 1) * B32);
+        for (int q = tid; q < KL * NB; q += kThreads) {
+          const int ll = q / NB, jj = q - (q / NB) * NB;
+          const int gl = l0 + ll, gj = j0 + jj;
+          dS[q] = (gl < k && gj < n) ? __ldg(Bt + (long long)gl * n + gj) : 0u;
+        }
+      }
       asm volatile("cp.async.commit_group;\n");
+    };
+
+    const long long g0 = g;
+    if (g0 >= NSTAGE) tc::mbar_wait(&mbar[g0 % NSTAGE], (uint32_t)(((g0 / NSTAGE) - 1) & 1));
+    issue_loads(0, g0);
+    for (int ch = 0; ch < nch; ++ch, ++g) {
+      const int s = (int)(g % NSTAGE);
+      if (ch + 1 < nch) {
+        const long long gn = g + 1;
+        // stage of chunk g+1 was last read by the MMAs of chunk g+1-NSTAGE
+        if (gn >= NSTAGE) tc::mbar_wait(&mbar[gn % NSTAGE], (uint32_t)(((gn / NSTAGE) - 1) & 1));
+        issue_loads(ch + 1, gn);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+      }
+      __syncthreads();  // chunk g's raw A tile and B block are visible
+      const uint32_t tA = sbase + s * STAGE, tB = tA + TILE_A;
+      uint8_t* pB = smem + s * STAGE + TILE_A;
+      const uint32_t* sBr =
+          reinterpret_cast<const uint32_t*>(smem + NSTAGE * STAGE + (g & 1) * B32);
       // ---- B tile: rows c = 4jj + r, bytes 4(l - l0) + q = byte r of s_q ----
       {
         const int jj = 8 * warp + (lane >> 2);
-        const int gj = j0 + jj;
-#pragma unroll 2
+#pragma unroll 4
         for (int u = 0; u < KL / 4; ++u) {
           const int ll = 4 * u + (lane & 3);
-          const int gl = l0 + ll;
-          uint32_t b = (gj < n && gl < k) ? __ldg(Bt + (long long)gl * n + gj) : 0u;
+          const uint32_t b = sBr[ll * NB + jj];
           const uint32_t s1 = d_red(d_shoup(b, pc.sc[1].x, pc.sc[1].y, p), p);
           const uint32_t s2 = d_red(d_shoup(b, pc.sc[2].x, pc.sc[2].y, p), p);
           const uint32_t s3 = d_red(d_shoup(b, pc.sc[3].x, pc.sc[3].y, p), p);
@@ -125,7 +166,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<uint32_t*>(pB + base + (rb + 3) * 16) = w3;
         }
       }
-      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
       tc::fence_proxy_async();
       __syncthreads();
       if (tid == 0) {
