@@ -28,6 +28,9 @@ def to_device(arr, p, device=None):
     """numpy (uint) array -> CUDA tensor in the storage dtype for p."""
     import torch
 
+    if not torch.cuda.is_available():
+        raise _lib.FpmBackendError(
+            "no CUDA device: the B200 product path has no CPU fallback")
     eb = elem_bytes_for(p)
     a = np.ascontiguousarray(arr, dtype=np.uint32 if eb == 4 else np.uint64)
     t = torch.from_numpy(a.view(np.int32 if eb == 4 else np.int64))
