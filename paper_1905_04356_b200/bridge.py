@@ -38,12 +38,15 @@ def install_into_reference(fpmat_pkg=None):
         "pmbasis": _wrap(RefPolMat, appint.pmbasis),
         "mbasis": _wrap(RefPolMat, appint.mbasis),
     }
-    saved = {}
+    # import every module first so none binds an already-replaced name
+    mods = []
     for mod in ("polmat", "appint", "kernel", "fraction", "solve"):
         try:
-            m = importlib.import_module(f"{name}.{mod}")
+            mods.append(importlib.import_module(f"{name}.{mod}"))
         except Exception:
             continue
+    saved = {}
+    for m in mods:
         for attr, fn in repl.items():
             if hasattr(m, attr):
                 saved[(m.__name__, attr)] = getattr(m, attr)
