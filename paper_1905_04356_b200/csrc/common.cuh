@@ -111,6 +111,16 @@ __device__ __forceinline__ uint32_t d_red64(uint64_t x, uint32_t p, uint64_t mu)
   return r >= p ? r32 - p : r32;
 }
 
+// x mod p for x < 2^56 and 2^30 <= p < 2^31, with m58 = floor(2^58 / p):
+// q = floor((x >> 26) m58 / 2^32) is floor(x/p) or one less (the dropped low
+// 26 bits and the truncation of m58 cost < 0.32), so x - q p lies in [0, 2p)
+// and its low 32 bits are exact.
+__device__ __forceinline__ uint32_t d_red56(uint64_t x, uint32_t p, uint32_t m58) {
+  const uint32_t q = __umulhi((uint32_t)(x >> 26), m58);
+  const uint32_t r = (uint32_t)x - q * p;
+  return min(r, r - p);
+}
+
 // Per-prime constants handed to kernels by value (kernel-parameter space, so
 // the radix-32 root constants are constant-bank operands, not loads).
 struct PrimeConst {
@@ -124,6 +134,7 @@ struct PrimeConst {
   uint2 w32[16];     // (w32^e, Shoup) e < 16, w32 = w^(N/32): inner radix-32 DFTs
   uint2 iw32[16];    // inverse roots
   uint2 sc[4];       // (2^(8q) mod p, Shoup), q = 0..3: limb scaling (tc_pointwise.cu)
+  uint32_t m58;      // floor(2^58 / p): reduction of < 2^56 limb sums (d_red56)
 };
 
 constexpr int kMaxPrimes = 8;

@@ -130,20 +130,24 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     __syncthreads();
     to_smem<LOGN, MAP_LAST>(smt, v, lt);
     __syncthreads();
-    constexpr int GQ = G::TPC / 4;
-    const bool vec = (a.n_entries & 3) == 0;
+    constexpr int PW = G::TPC < 4 ? G::TPC : 4;  // values per row piece
+    constexpr int GQ = G::TPC / PW;
+    const bool vec = (a.n_entries % PW) == 0;
     for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
       const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
-      const long long eb = e0 + 4 * gq;
-      uint32_t w[4];
+      const long long eb = e0 + PW * gq;
+      uint32_t w[PW];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) w[q] = sm[(4 * gq + q) * G::STRIDE + pad(x)];
+      for (int q = 0; q < PW; ++q) w[q] = sm[(PW * gq + q) * G::STRIDE + pad(x)];
       uint32_t* dst = out + (long long)x * a.n_entries + eb;
-      if (vec && eb + 3 < a.n_entries) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (vec && eb + PW - 1 < a.n_entries) {
+        if constexpr (PW == 4)
+          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        else
+          *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[PW - 1]);
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < PW; ++q)
           if (eb + q < a.n_entries) dst[q] = w[q];
       }
     }
@@ -160,10 +164,11 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     }
   } else {
     // eval layout: this thread owns point block lt (x = 32*lt + i)
-    uint4* dst = reinterpret_cast<uint4*>(out + ((long long)lt * a.n_entries + e) * 32);
+    const int pl = a.pblk_log ? a.pblk_log : 5;
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      *reinterpret_cast<uint4*>(out + eval_piece(lt * 32 + 4 * q, e, a.n_entries, pl)) =
+          make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
 }
 
@@ -194,30 +199,37 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     __syncthreads();
     from_smem<LOGN, MAP_LAST>(smt, v, lt);
   } else if (a.pm) {
-    constexpr int GQ = G::TPC / 4;
-    const bool vec = (a.n_entries & 3) == 0;
+    constexpr int PW = G::TPC < 4 ? G::TPC : 4;  // values per row piece
+    constexpr int GQ = G::TPC / PW;
+    const bool vec = (a.n_entries % PW) == 0;
     for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
       const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
-      const long long eb = e0 + 4 * gq;
+      const long long eb = e0 + PW * gq;
       const uint32_t* src = in + (long long)x * a.n_entries + eb;
-      uint32_t w[4];
-      if (vec && eb + 3 < a.n_entries) {
-        const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
-        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+      uint32_t w[PW];
+      if (vec && eb + PW - 1 < a.n_entries) {
+        if constexpr (PW == 4) {
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
+          w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+        } else {
+          const uint2 t = __ldg(reinterpret_cast<const uint2*>(src));
+          w[0] = t.x; w[PW - 1] = t.y;
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = eb + q < a.n_entries ? src[q] : 0u;
+        for (int q = 0; q < PW; ++q) w[q] = eb + q < a.n_entries ? src[q] : 0u;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) sm[(4 * gq + q) * G::STRIDE + pad(x)] = w[q];
+      for (int q = 0; q < PW; ++q) sm[(PW * gq + q) * G::STRIDE + pad(x)] = w[q];
     }
     __syncthreads();
     from_smem<LOGN, MAP_LAST>(smt, v, lt);
   } else if (valid) {
-    const uint4* src = reinterpret_cast<const uint4*>(in + ((long long)lt * a.n_entries + e) * 32);
+    const int pl = a.pblk_log ? a.pblk_log : 5;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const uint4 t = __ldg(src + q);
+      const uint4 t = __ldg(
+          reinterpret_cast<const uint4*>(in + eval_piece(lt * 32 + 4 * q, e, a.n_entries, pl)));
       v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
     }
   } else {
@@ -313,16 +325,17 @@ int fwd_launch(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
   return kOk;
 }
 
-// point-major launches: >= 4 (up to 8) transforms per CTA, <= 1024 threads
+// point-major launches: 512 threads per CTA (2048: 8, 4096: 4, 8192: 2
+// transforms -> 32/16/8-byte row pieces); N <= 1024 keeps the default TPC >= 8
 template <int LOGN>
 constexpr int pm_tpc() {
-  return (1 << LOGN) <= 1024 ? 0 : ((1 << LOGN) <= 4096 ? 8 : (1 << (15 - LOGN)));
+  return (1 << LOGN) <= 1024 ? 0 : (LOGN >= 14 ? 1 : (1 << (14 - LOGN)));
 }
 
 template <int LOGN>
 int fwd_impl(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
   if (a.pm) {
-    if constexpr (pm_tpc<LOGN>() >= 4 || pm_tpc<LOGN>() == 0) {
+    if constexpr (pm_tpc<LOGN>() >= 2 || pm_tpc<LOGN>() == 0) {
       return ps.count == 1 ? fwd_launch<LOGN, true, pm_tpc<LOGN>()>(a, ps, st)
                            : fwd_launch<LOGN, false, pm_tpc<LOGN>()>(a, ps, st);
     } else {
@@ -354,7 +367,7 @@ int inv_launch(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
 template <int LOGN>
 int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
   if (a.pm) {
-    if constexpr (pm_tpc<LOGN>() >= 4 || pm_tpc<LOGN>() == 0) {
+    if constexpr (pm_tpc<LOGN>() >= 2 || pm_tpc<LOGN>() == 0) {
       return ps.count == 1 ? inv_launch<LOGN, true, pm_tpc<LOGN>()>(a, ps, st)
                            : inv_launch<LOGN, false, pm_tpc<LOGN>()>(a, ps, st);
     } else {

@@ -35,6 +35,7 @@ struct NttFwdArgs {
   int reduce;                // inputs may be >= p: reduce on load
   int natural;               // 1: natural-order output out[e*N + k] (public API)
   int pm;                    // 1: point-major output out[x*n_entries + e]
+  int pblk_log;              // eval layout block: 0/5 -> E[N/32][E][32], 2 -> E[N/4][E][4]
   int n_entries;
   uint32_t* out;             // eval layout E[N/32][n_entries][32] (or natural / PM)
   long long out_prime_stride;
@@ -45,6 +46,7 @@ struct NttInvArgs {
   long long in_prime_stride;
   int natural;               // 1: natural-order input in[e*N + k] (public API)
   int pm;                    // 1: point-major input in[x*n_entries + e]
+  int pblk_log;              // eval layout block (as NttFwdArgs)
   int n_entries;
   uint32_t* out;             // out[e * out_stride + t] = coeff[(off + t) mod N]
   long long out_stride;
@@ -63,6 +65,13 @@ bool ntt_persist_fwd_ok(int logn, const NttFwdArgs& a);
 bool ntt_persist_inv_ok(int logn, const NttInvArgs& a);
 int launch_ntt_fwd_persist(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
 int launch_ntt_inv_persist(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
+
+// word offset of the 16-byte piece holding points x0 .. x0+3 (x0 % 4 == 0)
+// of entry e in the blocked eval layout E[N / 2^pl][n_entries][2^pl]
+__host__ __device__ __forceinline__ long long eval_piece(int x0, long long e, long long n_entries,
+                                                        int pl) {
+  return (((long long)(x0 >> pl) * n_entries + e) << pl) + (x0 & ((1 << pl) - 1));
+}
 
 constexpr int kMinLogN = 5;
 constexpr int kMaxLogN = 15;

@@ -7,17 +7,24 @@
 namespace fpm {
 namespace nttp {
 
-// PM (point-major output) launches use TPCX >= 4 transforms per CTA so each
-// evaluation point receives a >= 16-byte contiguous row segment.
+// PM (point-major output) launches use TPCX >= 2 transforms per CTA so each
+// evaluation point receives a >= 8-byte contiguous row segment.
+// TPCX == kPaired: two transforms per CTA on interleaved lanes (tr = lane & 1),
+// so the two values of one point meet in a lane pair (shuffle, no smem).
+constexpr int kPaired = 102;
+
 template <int LOGN, int TPCX = 0>
 struct Geo {
   static constexpr int N = 1 << LOGN;
   static constexpr int TPT = N / 32;                       // threads per transform
-  static constexpr int TPC = TPCX ? TPCX : (N >= 8192 ? 1 : 8192 / N);  // transforms per CTA
+  static constexpr bool PAIRED = TPCX == kPaired;
+  static constexpr int TPC = PAIRED ? 2 : (TPCX ? TPCX : (N >= 8192 ? 1 : 8192 / N));
   static constexpr int THREADS = TPT * TPC;                // 256 (N<=8192), 512, 1024
   static constexpr int NPASS = (LOGN + 4) / 5;             // 1, 2 or 3 passes
   static constexpr int LAST_R = LOGN - 5 * (NPASS - 1);    // bits of the last pass
-  static constexpr int STRIDE = N + N / 32;                // padded smem words / transform
+  // padded smem words / transform (+16 when paired: the two transforms of a
+  // warp then sit in opposite bank halves)
+  static constexpr int STRIDE = N + N / 32 + (PAIRED ? 16 : 0);
   static constexpr int SMEM_BYTES = TPC * STRIDE * 4;
 };
 

@@ -10,6 +10,8 @@
 //     butterfly work instead of stalling it.
 // Forward: u32 input (no fold / no reduction), blocked-eval or point-major
 // output.  Inverse: blocked-eval or point-major input.
+#include <cstdlib>
+
 #include "ntt.cuh"
 #include "ntt_passes.cuh"
 
@@ -117,7 +119,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   const int z = SINGLE ? 0 : blockIdx.z;
   const PrimeConst& pc = ps.pr[z];
   const int tid = threadIdx.x;
-  const int tr = tid / G::TPT, lt = tid % G::TPT;
+  const int tr = G::PAIRED ? (tid & 1) : tid / G::TPT;
+  const int lt = G::PAIRED ? (tid >> 1) : tid % G::TPT;
   uint32_t* smt = sm + tr * G::STRIDE;
   const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
   const uint32_t* in = (const uint32_t*)a.in + (long long)z * a.in_prime_stride;
@@ -171,32 +174,64 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     if (kPrefetch && nxt < groups) load_group(nxt);  // in flight during the passes
     fwd_passes<LOGN, TPCX>(v, smt, tws, pc, lt, upper_zero);
     const long long e0 = grp * G::TPC, e = e0 + tr;
-    if (a.pm) {
+    if (G::PAIRED && a.pm) {
+      // lane pair (tr = 0, 1) holds the two transforms of the same 32 points:
+      // exchange half of them so each lane writes (T0[x], T1[x]) as 8 bytes
+      const bool vec = (a.n_entries & 1) == 0 && e0 + 1 < a.n_entries;
+#pragma unroll
+      for (int i = 0; i < 32; i += 2) {
+        const uint32_t send = tr ? v[i] : v[i + 1];
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        const int x = xmap<LOGN, MAP_LAST>(lt, i + tr);
+        const uint32_t lo = tr ? recv : v[i], hi = tr ? v[i + 1] : recv;
+        uint32_t* dst = out + (long long)x * a.n_entries + e0;
+        if (vec) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
+        } else {
+          if (e0 < a.n_entries) dst[0] = lo;
+          if (e0 + 1 < a.n_entries) dst[1] = hi;
+        }
+      }
+    } else if (G::TPC == 1 && a.pm) {
+      // point-major scatter straight from registers (4-byte pieces; the
+      // other entries of each 32-byte sector come from neighbouring CTAs)
+      if (e < a.n_entries) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          out[(long long)xmap<LOGN, MAP_LAST>(lt, i) * a.n_entries + e] = v[i];
+      }
+    } else if (a.pm) {
       __syncthreads();
       to_smem<LOGN, MAP_LAST>(smt, v, lt);
       __syncthreads();
-      constexpr int GQ = G::TPC / 4;
-      const bool vec = (a.n_entries & 3) == 0;
+      constexpr int PW = G::TPC < 4 ? G::TPC : 4;  // values per row piece
+      constexpr int GQ = G::TPC / PW;
+      const bool vec = (a.n_entries % PW) == 0;
+#pragma unroll 8
       for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
         const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
-        const long long eb = e0 + 4 * gq;
-        uint32_t w[4];
+        const long long eb = e0 + PW * gq;
+        uint32_t w[PW];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) w[q] = sm[(4 * gq + q) * G::STRIDE + pad(x)];
+        for (int q = 0; q < PW; ++q) w[q] = sm[(PW * gq + q) * G::STRIDE + pad(x)];
         uint32_t* dst = out + (long long)x * a.n_entries + eb;
-        if (vec && eb + 3 < a.n_entries) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (vec && eb + PW - 1 < a.n_entries) {
+          if constexpr (PW == 4)
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+          else
+            *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[PW - 1]);
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < PW; ++q)
             if (eb + q < a.n_entries) dst[q] = w[q];
         }
       }
     } else if (e < a.n_entries) {
-      uint4* dst = reinterpret_cast<uint4*>(out + ((long long)lt * a.n_entries + e) * 32);
+      const int pl = a.pblk_log ? a.pblk_log : 5;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        dst[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        *reinterpret_cast<uint4*>(out + eval_piece(lt * 32 + 4 * q, e, a.n_entries, pl)) =
+            make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     __syncthreads();  // smem exchange buffer reused by the next group
     if (!kPrefetch && nxt < groups) load_group(nxt);
@@ -213,43 +248,74 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   const PrimeConst& pc = ps.pr[z];
   const uint32_t p = pc.p;
   const int tid = threadIdx.x;
-  const int tr = tid / G::TPT, lt = tid % G::TPT;
+  const int tr = G::PAIRED ? (tid & 1) : tid / G::TPT;
+  const int lt = G::PAIRED ? (tid >> 1) : tid % G::TPT;
   uint32_t* smt = sm + tr * G::STRIDE;
   const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
   const uint32_t* in = a.in + (long long)z * a.in_prime_stride;
   uint32_t* out = a.out + (long long)z * a.out_prime_stride;
   constexpr int FINAL = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
-  constexpr int GQ = G::TPC / 4;
+  constexpr int PW = G::TPC < 4 ? G::TPC : 4;  // point-major row piece (values)
+  constexpr int GQ = G::TPC / PW;
 
   stage_table<LOGN>(tws, pc.itw);
 
   uint32_t pre[32];
   auto load_group = [&](long long grp) {
     const long long e0 = grp * G::TPC;
-    if (a.pm) {
-      // this thread's share of the group's point-major input: 16-byte pieces
-      const bool vec = (a.n_entries & 3) == 0;
+    if (G::PAIRED && a.pm) {
+      // raw (T0[x], T1[x]) pairs for x = point of element i + tr; swapped
+      // into place when the group is consumed
+      const bool vec = (a.n_entries & 1) == 0 && e0 + 1 < a.n_entries;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int i = 0; i < 32; i += 2) {
+        const int x = xmap<LOGN, MAP_LAST>(lt, i + tr);
+        const uint32_t* src = in + (long long)x * a.n_entries + e0;
+        if (vec) {
+          const uint2 t = __ldg(reinterpret_cast<const uint2*>(src));
+          pre[i] = t.x; pre[i + 1] = t.y;
+        } else {
+          pre[i] = e0 < a.n_entries ? src[0] : 0u;
+          pre[i + 1] = e0 + 1 < a.n_entries ? src[1] : 0u;
+        }
+      }
+    } else if (G::TPC == 1 && a.pm) {
+      const long long e = e0 + tr;
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        pre[i] = e < a.n_entries
+                     ? __ldg(in + (long long)xmap<LOGN, MAP_LAST>(lt, i) * a.n_entries + e)
+                     : 0u;
+    } else if (a.pm) {
+      // this thread's share of the group's point-major input: PW-value pieces
+      const bool vec = (a.n_entries % PW) == 0;
+#pragma unroll
+      for (int u = 0; u < 32 / PW; ++u) {
         const int idx = tid + u * G::THREADS;
         const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
-        const long long eb = e0 + 4 * gq;
+        const long long eb = e0 + PW * gq;
         const uint32_t* src = in + (long long)x * a.n_entries + eb;
-        if (vec && eb + 3 < a.n_entries) {
-          const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
-          pre[4 * u] = t.x; pre[4 * u + 1] = t.y; pre[4 * u + 2] = t.z; pre[4 * u + 3] = t.w;
+        if (vec && eb + PW - 1 < a.n_entries) {
+          if constexpr (PW == 4) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(src));
+            pre[4 * u] = t.x; pre[4 * u + 1] = t.y; pre[4 * u + 2] = t.z; pre[4 * u + 3] = t.w;
+          } else {
+            const uint2 t = __ldg(reinterpret_cast<const uint2*>(src));
+            pre[PW * u] = t.x; pre[PW * u + PW - 1] = t.y;
+          }
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) pre[4 * u + q] = eb + q < a.n_entries ? src[q] : 0u;
+          for (int q = 0; q < PW; ++q) pre[PW * u + q] = eb + q < a.n_entries ? src[q] : 0u;
         }
       }
     } else {
       const long long e = e0 + tr;
       if (e < a.n_entries) {
-        const uint4* src = reinterpret_cast<const uint4*>(in + ((long long)lt * a.n_entries + e) * 32);
+        const int pl = a.pblk_log ? a.pblk_log : 5;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const uint4 t = __ldg(src + q);
+          const uint4 t = __ldg(reinterpret_cast<const uint4*>(
+              in + eval_piece(lt * 32 + 4 * q, e, a.n_entries, pl)));
           pre[4 * q] = t.x; pre[4 * q + 1] = t.y; pre[4 * q + 2] = t.z; pre[4 * q + 3] = t.w;
         }
       } else {
@@ -264,13 +330,22 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   __syncthreads();
   for (; grp < groups; grp += gridDim.x) {
     uint32_t v[32];
-    if (a.pm) {
+    if (G::PAIRED && a.pm) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int i = 0; i < 32; i += 2) {
+        // pre[i..i+1] = (T0, T1) at point i + tr; this lane wants T_tr at i, i+1
+        const uint32_t send = tr ? pre[i] : pre[i + 1];
+        const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        v[i] = tr ? recv : pre[i];
+        v[i + 1] = tr ? pre[i + 1] : recv;
+      }
+    } else if (a.pm && G::TPC > 1) {
+#pragma unroll
+      for (int u = 0; u < 32 / PW; ++u) {
         const int idx = tid + u * G::THREADS;
         const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) sm[(4 * gq + q) * G::STRIDE + pad(x)] = pre[4 * u + q];
+        for (int q = 0; q < PW; ++q) sm[(PW * gq + q) * G::STRIDE + pad(x)] = pre[PW * u + q];
       }
       __syncthreads();
       from_smem<LOGN, MAP_LAST>(smt, v, lt);
@@ -315,10 +390,11 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   }
 }
 
-// point-major: 4 transforms per CTA (16-byte row pieces), <= 512 threads for N <= 4096
+// point-major: 4 transforms per CTA (16-byte row pieces) for N = 4096, 2
+// (8-byte pieces) for N = 8192 so a CTA stays at 512 threads / 128 registers
 template <int LOGN>
 constexpr int pm_tpc2() {
-  return (1 << LOGN) <= 2048 ? 0 : 4;
+  return (1 << LOGN) <= 2048 ? 0 : ((1 << LOGN) <= 4096 ? 4 : kPaired);
 }
 
 template <int LOGN, bool SINGLE, int TPCX, bool FWD, typename Args>
@@ -355,6 +431,11 @@ int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
 
 template <int LOGN, bool FWD, typename Args>
 int persist_impl(const Args& a, const PrimeSet& ps, cudaStream_t st) {
+  static const bool pm_scatter = std::getenv("FPM_PM_SCATTER") != nullptr;
+  if (a.pm && pm_scatter && (1 << LOGN) >= 256) {
+    return ps.count == 1 ? persist_launch<LOGN, true, 1, FWD>(a, ps, st)
+                         : persist_launch<LOGN, false, 1, FWD>(a, ps, st);
+  }
   if (a.pm) {
     return ps.count == 1 ? persist_launch<LOGN, true, pm_tpc2<LOGN>(), FWD>(a, ps, st)
                          : persist_launch<LOGN, false, pm_tpc2<LOGN>(), FWD>(a, ps, st);

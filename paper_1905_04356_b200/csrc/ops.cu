@@ -146,14 +146,23 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
 
   const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
   // large contractions: int8 tensor-core pointwise on point-major operands
+  // small matrices (m <= 128): grouped TMA-fed kernel, G points per UMMA tile
   static const bool tc_off = std::getenv("FPM_DISABLE_TC") != nullptr;
+  static const bool small_off = std::getenv("FPM_DISABLE_TC_SMALL") != nullptr;
+  static const bool pq_off = std::getenv("FPM_DISABLE_TC_PQ") != nullptr;
+  bool pq = !tc_off && !pq_off && logn <= 13 && (long long)m * k * n >= 4096;
+  for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
+  bool grouped = !pq && !tc_off && !small_off && logn <= 13 && (long long)m * k * n >= 4096;
+  for (int i = 0; i < r && grouped; ++i) grouped = tc_grouped_applicable(m, k, n, primes[i]);
   bool use_tc = !tc_off && logn <= 13;
   for (int i = 0; i < r && use_tc; ++i) use_tc = tc_pointwise_applicable(m, k, n, primes[i]);
+  use_tc = !pq && (use_tc || grouped);
   // forward transforms (all primes in one launch: blockIdx.z = prime)
   NttFwdArgs fa{};
   fa.in = A.ptr; fa.in64 = A.is64; fa.in_stride = A.stride; fa.in_prime_stride = 0;
   fa.len = A.len; fa.fold = 0; fa.reduce = reduce_needed || (!direct && A.is64);
-  fa.natural = 0; fa.pm = use_tc; fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
+  fa.natural = 0; fa.pm = use_tc; fa.pblk_log = pq ? 2 : 5;
+  fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
   if (direct && A.is64) fa.reduce = 0;
   {
     StageTimer t_(cx, "ntt_fwd_A");
@@ -169,12 +178,21 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
   }
 
-  if (use_tc) {
+  if (pq) {
     TcArgs ta{};
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
     ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
     StageTimer t_(cx, "pointwise_tc");
-    FPM_TRY(launch_tc_pointwise(ta, ps, st));
+    FPM_TRY(launch_tc_pq(ta, ps, st));
+  } else if (use_tc) {
+    TcArgs ta{};
+    ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
+    ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
+    StageTimer t_(cx, "pointwise_tc");
+    if (grouped)
+      FPM_TRY(launch_tc_grouped(ta, ps, st));
+    else
+      FPM_TRY(launch_tc_pointwise(ta, ps, st));
   } else {
     PointwiseArgs pa{};
     pa.A = EA; pa.B = EB; pa.C = EC; pa.m = m; pa.k = k; pa.n = n; pa.nblk = (int)(N / 32);
@@ -185,6 +203,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
 
   NttInvArgs ia{};
   ia.in = EC; ia.in_prime_stride = N * ec; ia.natural = 0; ia.pm = use_tc; ia.n_entries = (int)ec;
+  ia.pblk_log = pq ? 2 : 5;
   ia.out_len = wlen; ia.off = (int)off; ia.scale = 1;
   if (direct && !C.is64) {
     ia.out = (uint32_t*)C.ptr; ia.out_stride = C.stride; ia.out_prime_stride = 0;

@@ -262,6 +262,7 @@ int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   out->p = p;
   out->c32 = (uint32_t)(((uint64_t)1 << 32) % p);
   out->mu = (uint64_t)((((u128)1) << 64) / p);
+  out->m58 = (uint32_t)((((u128)1) << 58) / p);
   out->ninv = pl->ninv;
   out->ninv_sh = pl->ninv_sh;
   for (int q = 0; q < 4; ++q) {

@@ -27,6 +27,20 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// UMMA descriptor for a K-major SWIZZLE_128B tile (rows of 128 B, 8-row
+// atoms of 1024 B, the layout a TMA box with CU_TENSOR_MAP_SWIZZLE_128B
+// writes).  The tile base must be 1024-byte aligned; advancing along K inside
+// the 128-byte atom adds the byte offset to the start address.
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // layout type SWIZZLE_128B
+  return d;
+}
+
 // instruction descriptor: kind::i8, u8 x u8 -> s32, both operands K-major
 __host__ __device__ constexpr uint32_t idesc_u8(int M, int N) {
   return (2u << 4)                       // D format S32
@@ -61,6 +75,51 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
       "@!done bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
       "r"(parity));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
+}
+// 4-D tiled TMA load global -> shared, completion on an mbarrier (tx bytes)
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const void* tmap, uint64_t* mbar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(mbar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// same, on a precomputed shared-memory address; the suspend-time hint lets
+// the warp sleep in the barrier instead of re-issuing try_wait
+__device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, %2;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(addr),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_a(uint32_t addr) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void commit_a(uint32_t addr) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          addr)
+      : "memory");
 }
 
 __device__ __forceinline__ void fence_proxy_async() {

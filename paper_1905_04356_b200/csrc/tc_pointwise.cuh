@@ -16,4 +16,13 @@ struct TcArgs {
 bool tc_pointwise_applicable(int m, int k, int n, uint32_t p);
 int launch_tc_pointwise(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// small matrices (m <= 128): G = 128/mp points per UMMA tile, TMA-fed,
+// warp-specialised (tc_grouped.cu)
+bool tc_grouped_applicable(int m, int k, int n, uint32_t p);
+int launch_tc_grouped(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
+
+// m <= 32 on the point-quad eval layout X[t/4][entry][t%4] (tc_pq.cu)
+bool tc_pq_applicable(int m, int k, int n, int npts, uint32_t p);
+int launch_tc_pq(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 }  // namespace fpm

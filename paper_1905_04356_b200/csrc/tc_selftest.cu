@@ -106,3 +106,54 @@ extern "C" int fpm_selftest_tc_pointwise(fpm_context* ctx, uint32_t p, const voi
   FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
   return kOk;
 }
+
+// grouped small-matrix kernel for tests: for prime z < nprimes and t < npts,
+// C[z][t] = A[z][t] B[z][t] mod primes[z] (point-major, primes stacked)
+extern "C" int fpm_selftest_tc_grouped(fpm_context* ctx, const uint32_t* primes, int nprimes,
+                                       const void* A, const void* B, void* C, int m, int k,
+                                       int n, int npts) {
+  using namespace fpm;
+  if (!ctx || nprimes < 1 || nprimes > 8) {
+    set_last_error("tc_grouped selftest: bad arguments");
+    return kInvalidArgument;
+  }
+  PrimeSet ps;
+  ps.count = nprimes;
+  for (int i = 0; i < nprimes; ++i) {
+    if (!tc_grouped_applicable(m, k, n, primes[i])) {
+      set_last_error("tc_grouped not applicable to m=%d k=%d n=%d", m, k, n);
+      return kInvalidArgument;
+    }
+    FPM_TRY(ctx->cx->prime_const(primes[i], 5, &ps.pr[i]));
+  }
+  TcArgs a{};
+  a.A = (const uint32_t*)A; a.B = (const uint32_t*)B; a.C = (uint32_t*)C;
+  a.m = m; a.k = k; a.n = n; a.npts = npts;
+  a.a_ps = (long long)npts * m * k; a.b_ps = (long long)npts * k * n;
+  a.c_ps = (long long)npts * m * n;
+  FPM_TRY(launch_tc_grouped(a, ps, ctx->cx->stream()));
+  FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
+  return kOk;
+}
+
+// point-quad kernel for tests: operands in the eval layout X[z][t/4][entry][t%4]
+extern "C" int fpm_selftest_tc_pq(fpm_context* ctx, const uint32_t* primes, int nprimes,
+                                  const void* A, const void* B, void* C, int m, int k, int n,
+                                  int npts) {
+  using namespace fpm;
+  if (!ctx || nprimes < 1 || nprimes > 8) {
+    set_last_error("tc_pq selftest: bad arguments");
+    return kInvalidArgument;
+  }
+  PrimeSet ps;
+  ps.count = nprimes;
+  for (int i = 0; i < nprimes; ++i) FPM_TRY(ctx->cx->prime_const(primes[i], 5, &ps.pr[i]));
+  TcArgs a{};
+  a.A = (const uint32_t*)A; a.B = (const uint32_t*)B; a.C = (uint32_t*)C;
+  a.m = m; a.k = k; a.n = n; a.npts = npts;
+  a.a_ps = (long long)npts * m * k; a.b_ps = (long long)npts * k * n;
+  a.c_ps = (long long)npts * m * n;
+  FPM_TRY(launch_tc_pq(a, ps, ctx->cx->stream()));
+  FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
+  return kOk;
+}
