@@ -149,10 +149,15 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // small matrices (m <= 128): grouped TMA-fed kernel, G points per UMMA tile
   static const bool tc_off = std::getenv("FPM_DISABLE_TC") != nullptr;
   static const bool small_off = std::getenv("FPM_DISABLE_TC_SMALL") != nullptr;
+  // point-quad TC kernel for 16 < m <= 32 (cfg2: 0.205 vs 0.225 ms on the
+  // CUDA cores); m <= 16 stays on the CUDA cores (cfg3: 35 vs 75 us)
   static const bool pq_off = std::getenv("FPM_DISABLE_TC_PQ") != nullptr;
-  bool pq = !tc_off && !pq_off && logn <= 13 && (long long)m * k * n >= 4096;
+  bool pq = !tc_off && !pq_off && logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
   for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
-  bool grouped = !pq && !tc_off && !small_off && logn <= 13 && (long long)m * k * n >= 4096;
+  // grouped PM-layout TC kernel: for 32 < m <= 128 (m <= 32 stays on the
+  // CUDA cores, whose blocked layout keeps the NTTs at full speed)
+  bool grouped = !pq && !tc_off && !small_off && logn <= 13 && m > 32 &&
+                 (long long)m * k * n >= 4096;
   for (int i = 0; i < r && grouped; ++i) grouped = tc_grouped_applicable(m, k, n, primes[i]);
   bool use_tc = !tc_off && logn <= 13;
   for (int i = 0; i < r && use_tc; ++i) use_tc = tc_pointwise_applicable(m, k, n, primes[i]);
