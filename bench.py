@@ -171,6 +171,105 @@ def read_traffic():
 
 
 # ---------------------------------------------------------------------------
+def read_int8_peak():
+    """Measured int8 tensor-core peak (tools/int8_peak.py on this pool's B200:
+    torch._int_mm 8192^3), TOPS; sustained figure for kernels inside a step."""
+    path = os.path.join(ROOT, "profiles", "int8_peak.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["int8_tops_sustained"]), "measured (profiles/int8_peak.json, sustained)"
+    except Exception:
+        return 4500.0, "nominal dense int8 4.5 POPS"
+
+
+def tc_ops(cfg):
+    """(useful, issued) int8 ops of the tensor-core pointwise stage, mirroring
+    the kernel choice in ops.cu cyclic_product; None when it runs on CUDA cores."""
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    N, r = mul_plan(cfg)
+    pts = N * r
+    useful = 2 * 16 * m * k * n * pts
+    if m * k * n < 4096 or N > 8192:
+        return None
+    nch = -(-k // 32)
+
+    def pow2(x, lo, hi):
+        v = lo
+        while v < x and v < hi:
+            v *= 2
+        return v
+
+    if 16 < m <= 32:                       # tc_pq.cu
+        nb = pow2(n, 8, 32)
+        per = 2 * 128 * 4 * nb * 128 * nch * -(-n // nb)
+    elif 32 < m <= 128 and k % 4 == 0 and n % 4 == 0:   # tc_grouped.cu
+        mp = pow2(m, 16, 128)
+        nb = pow2(n, 8, min(mp, 64))
+        per = 2 * 128 * 4 * nb * 128 * nch * -(-n // nb)
+    elif m >= 64 and k % 4 == 0 and 64 <= k <= 8192 and n >= 32:  # tc_pointwise.cu
+        per = 2 * 256 * -(-m // 256) * 256 * -(-n // 64) * 128 * nch
+    else:
+        return None
+    return useful, per * pts
+
+
+def roofline_report(cfg, cfgname, avg, sbytes):
+    """Roofline of the dominant kernel class (NTT = the forward and inverse
+    transform launches, pointwise, CRT) plus a per-stage table.  Bytes are
+    SURVEY.md 8(d)'s algorithmic per-stage bytes; `traffic` is ncu
+    dram__bytes_read.sum + dram__bytes_write.sum of the same launches
+    (profiles/ncu_traffic.json)."""
+    hbm, hsrc = read_peaks()
+    i8, i8src = read_int8_peak()
+    traffic = read_traffic().get(cfgname, {})
+
+    def tr(stage):
+        key = "ntt_fwd" if stage.startswith("ntt_fwd") else stage
+        v = traffic.get(key)
+        return round(sum(v) / len(v)) if v else None
+
+    table = {}
+    for st, ms in avg.items():
+        b = sbytes.get("pointwise" if st.startswith("pointwise") else st)
+        if b is None:
+            continue
+        ach = b / (ms * 1e-3) / 1e9
+        ent = {"ms": round(ms, 5), "bound": "hbm", "achieved": round(ach, 1), "peak": hbm,
+               "unit": "GB/s", "frac": round(ach / hbm, 4), "algorithmic_bytes": b,
+               "traffic": tr(st)}
+        if st == "pointwise_tc":
+            ops = tc_ops(cfg)
+            if ops:
+                ent["tensor"] = {"useful_tops": round(ops[0] / (ms * 1e-3) / 1e12, 1),
+                                 "issued_tops": round(ops[1] / (ms * 1e-3) / 1e12, 1),
+                                 "peak_tops": i8, "frac_issued": round(ops[1] / (ms * 1e-3) / 1e12 / i8, 4),
+                                 "peak_source": i8src}
+        table[st] = ent
+    classes = {"ntt": [s for s in table if s.startswith("ntt")],
+               "pointwise": [s for s in table if s.startswith("pointwise")],
+               "crt": [s for s in table if s == "crt"]}
+    dom = max(classes, key=lambda c: sum(avg[s] for s in classes[c]))
+    members = classes[dom]
+    ms = sum(avg[s] for s in members)
+    b = sum(table[s]["algorithmic_bytes"] for s in members)
+    trs = [table[s]["traffic"] for s in members]
+    ach = b / (ms * 1e-3) / 1e9
+    roof = {"kernel": dom, "launches": members, "bound": "hbm", "achieved": round(ach, 1),
+            "peak": hbm, "unit": "GB/s", "frac": round(ach / hbm, 4),
+            "traffic": sum(trs) if all(t is not None for t in trs) else None,
+            "algorithmic_bytes": b, "ms": round(ms, 5), "peak_source": hsrc}
+    if dom == "ntt":
+        roof["note"] = ("HBM fraction per SURVEY 8(d); the NTT kernels are integer-ALU/issue "
+                        "bound (~7 instructions per butterfly), see DESIGN.md")
+    if dom == "pointwise" and "pointwise_tc" in table and "tensor" in table["pointwise_tc"]:
+        t = table["pointwise_tc"]["tensor"]
+        roof.update({"bound": "tensor", "achieved": t["issued_tops"], "peak": i8,
+                     "unit": "TFLOP/s", "frac": t["frac_issued"], "peak_source": i8src,
+                     "note": "int8 ops issued (incl. grouping padding) / measured int8 peak"})
+    return roof, table
+
+
 def make_inputs(cfg, device, seed):
     import torch
 
@@ -433,19 +532,13 @@ def main():
         "gpu_launches": launches,
         "clocks": clk,
     }
-    # roofline of the dominant kernel stage, CUDA events inside the timed region
+    # roofline of the dominant kernel class, CUDA events inside the timed region
     if stages:
         avg = {k: sum(v) / len(v) for k, v in stages.items()}
         line["stages_ms"] = {k: round(v, 5) for k, v in avg.items()}
-        dom = max(avg, key=avg.get)
-        peak, peak_src = read_peaks()
-        if dom in sbytes:
-            ach = sbytes[dom] / (avg[dom] * 1e-3) / 1e9
-            traffic = read_traffic().get(args.config, {}).get(dom)
-            line["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1),
-                                "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                                "traffic": traffic, "algorithmic_bytes": sbytes[dom],
-                                "peak_source": peak_src}
+        if cfg["kind"] == "mul":
+            line["roofline"], line["roofline_stages"] = roofline_report(cfg, args.config, avg,
+                                                                        sbytes)
     if rank == 0 and not args.no_extras and cfg["kind"] == "mul":
         try:
             med, bi, bo = e2e_mul(cfg, max(3, args.steps // 2), 2, 7)

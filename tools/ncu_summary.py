@@ -31,7 +31,8 @@ METRICS = [
 ]
 
 STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_inv": "ntt_inv", "pointwise_cc": "pointwise",
-            "tc_pointwise": "pointwise_tc", "tc_grouped": "pointwise_tc"}
+            "tc_pointwise": "pointwise_tc", "tc_grouped": "pointwise_tc", "tc_pq": "pointwise_tc",
+            "crt_kernel": "crt"}
 
 
 def short(name):
@@ -95,7 +96,7 @@ def full(path, key=None):
     if key:
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         cur = json.load(open(tp)) if os.path.exists(tp) else {}
-        ent = cur.setdefault(key, {})
+        ent = cur[key] = {}  # replaced by this capture
         for rec in res:
             stage = next((v for k, v in STAGE_OF.items() if k in rec["kernel"]), None)
             if stage and "dram__bytes_read.sum" in rec:
