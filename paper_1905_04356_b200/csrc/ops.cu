@@ -154,8 +154,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   static const bool pq_off = std::getenv("FPM_DISABLE_TC_PQ") != nullptr;
   bool pq = !tc_off && !pq_off && logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
   for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
-  // grouped PM-layout TC kernel: for 32 < m <= 128 (m <= 32 stays on the
-  // CUDA cores, whose blocked layout keeps the NTTs at full speed)
+  // grouped / M-tiled PM-layout TC kernel (TMA, warp specialised) for m > 32;
+  // tc_pointwise.cu remains for shapes it does not take (p < 2^30)
   bool grouped = !pq && !tc_off && !small_off && logn <= 13 && m > 32 &&
                  (long long)m * k * n >= 4096;
   for (int i = 0; i < r && grouped; ++i) grouped = tc_grouped_applicable(m, k, n, primes[i]);

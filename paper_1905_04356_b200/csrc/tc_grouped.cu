@@ -57,6 +57,7 @@ struct GArgs {
   long long c_ps;
   int mp, G, nblk, ngroups, nch;
   int nring, nacc;
+  int mtiles;       // 128-row M tiles per point (m > 128: G = 1)
 };
 
 // position in a ring of mbarrier-guarded buffers (index + phase bit)
@@ -71,12 +72,15 @@ struct RingPos {
   }
 };
 
-__device__ __forceinline__ void decode(const GArgs& a, int it, int& z, int& gi, int& jb) {
-  const int per_z = a.ngroups * a.nblk;
+__device__ __forceinline__ void decode(const GArgs& a, int it, int& z, int& gi, int& mt,
+                                       int& jb) {
+  const int per_z = a.ngroups * a.mtiles * a.nblk;
   z = it / per_z;
   const int rem = it - z * per_z;
-  gi = rem / a.nblk;
-  jb = rem - gi * a.nblk;
+  const int gm = rem / a.nblk;
+  jb = rem - gm * a.nblk;
+  gi = gm / a.mtiles;
+  mt = gm - gi * a.mtiles;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t a_afull = tc::smem_u32(afull), a_aempty = tc::smem_u32(aempty);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = a.G, nch = a.nch, nring = a.nring, nacc = a.nacc;
-  const int items = a.nz * a.ngroups * a.nblk;  // < 2^31 (host-checked)
+  const int items = a.nz * a.ngroups * a.mtiles * a.nblk;  // < 2^31 (host-checked)
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
@@ -139,13 +143,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t bytes = kTileA + (uint32_t)(128 * NB * G);
       RingPos st{0, 0};
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        int z, gi, jb;
-        decode(a, it, z, gi, jb);
+        int z, gi, mt, jb;
+        decode(a, it, z, gi, mt, jb);
         for (int ch = 0; ch < nch; ++ch, st.next(NS)) {
           const int s = st.idx;
           tc::mbar_wait_a(a_empty + 8 * s, st.ph ^ 1u);
           tc::mbar_expect_tx(&full[s], bytes);
-          tc::tma_load_4d(sbase + s * kTileA, &tmA, &full[s], ch * 32, 0, gi * G, z);
+          tc::tma_load_4d(sbase + s * kTileA, &tmA, &full[s], ch * 32, mt * 128, gi * G, z);
           tc::tma_load_4d(sbase + kOffRaw + s * kRawB, &tmB, &full[s], jb * NB, ch * 32, gi * G,
                           z);
         }
@@ -192,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int sub = nacc / G;                   // slots per point
       RingPos sp0{0, 0}, sp1{0, 0};
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
-        int z, gi, jb;
-        decode(a, it, z, gi, jb);
+        int z, gi, mt, jb;
+        decode(a, it, z, gi, mt, jb);
         const uint32_t p = ps.pr[z].p;
         const uint32_t m58 = ps.pr[z].m58;
         const int j0 = jb * NB;
@@ -205,9 +209,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int slot = r.idx * G + g;
           tc::mbar_wait_a(a_afull + 8 * slot, r.ph);
           tc::fence_after_sync();
-          const int i = 32 * q + lane - g * a.mp;
+          const int il = 32 * q + lane - g * a.mp;  // row within the point's tile
+          const int i = mt * 128 + il;
           const int t = gi * G + g;
-          const bool ok = i >= 0 && i < a.m && t < a.npts;
+          const bool ok = il >= 0 && il < a.mp && i < a.m && t < a.npts;
           uint32_t* Crow = a.C + z * a.c_ps + ((long long)t * a.m + (ok ? i : 0)) * a.n;
 #pragma unroll 1
           for (int cc = 0; cc < kLoads; ++cc) {
@@ -250,8 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* smem = smem_raw + (sbase - sraw);
     RingPos st{0, 0}, br{0, 0};
     for (int it = blockIdx.x; it < items; it += gridDim.x) {
-      int z, gi, jb;
-      decode(a, it, z, gi, jb);
+      int z, gi, mt, jb;
+      decode(a, it, z, gi, mt, jb);
       const PrimeConst& pc = ps.pr[z];
       const uint32_t p = pc.p;
       const uint32_t w1 = pc.sc[1].x, w1p = pc.sc[1].y, w2 = pc.sc[2].x, w2p = pc.sc[2].y;
@@ -356,7 +361,7 @@ int launch_nb(const CUtensorMap& mA, const CUtensorMap& mB, const GArgs& a, cons
 }  // namespace
 
 bool tc_grouped_applicable(int m, int k, int n, uint32_t p) {
-  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && m <= 128 && k >= 1 && (k % 4) == 0 && n >= 1 &&
+  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && k >= 1 && (k % 4) == 0 && n >= 1 &&
          (n % 4) == 0;
 }
 
@@ -370,8 +375,9 @@ int launch_tc_grouped(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
   a.C = t.C; a.m = t.m; a.k = t.k; a.n = t.n; a.npts = t.npts; a.nz = ps.count;
   a.c_ps = t.c_ps;
   a.mp = 16;
-  while (a.mp < t.m) a.mp <<= 1;
+  while (a.mp < t.m && a.mp < 128) a.mp <<= 1;
   a.G = 128 / a.mp;
+  a.mtiles = (t.m + 127) / 128;  // > 1 only with mp = 128, G = 1
   // NB: power of two in [8, 64], <= mp so G accumulators of 4 NB columns fit TMEM
   int nb = 8;
   while (nb < t.n && nb < 64) nb <<= 1;
@@ -391,7 +397,7 @@ int launch_tc_grouped(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
     const uint64_t dims[4] = {(uint64_t)t.k, (uint64_t)t.m, (uint64_t)t.npts, nz};
     const uint64_t pstride = (uint64_t)(t.a_ps ? t.a_ps : (long long)t.npts * t.m * t.k) * 4;
     const uint64_t strides[3] = {(uint64_t)t.k * 4, (uint64_t)t.m * t.k * 4, pstride};
-    const uint32_t box[4] = {32, (uint32_t)a.mp, (uint32_t)a.G, 1};
+    const uint32_t box[4] = {32, (uint32_t)a.mp, (uint32_t)a.G, 1};  // mp <= 128 rows
     FPM_TRY(make_map(&mA, t.A, dims, strides, box, true));
   }
   {
@@ -401,7 +407,7 @@ int launch_tc_grouped(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
     const uint32_t box[4] = {(uint32_t)nb, 32, (uint32_t)a.G, 1};
     FPM_TRY(make_map(&mB, t.B, dims, strides, box, false));
   }
-  const long long items = (long long)ps.count * a.ngroups * a.nblk;
+  const long long items = (long long)ps.count * a.ngroups * a.mtiles * a.nblk;
   if (items >= (1LL << 31)) {
     set_last_error("tc_grouped: too many work items");
     return kUnsupported;

@@ -62,7 +62,8 @@ def test_tc_pointwise_exact(m, k, n):
 
 
 GROUPED_SHAPES = [(32, 32, 32, 13), (16, 16, 16, 40), (64, 64, 32, 9), (128, 64, 64, 3),
-                  (20, 36, 44, 11), (100, 100, 72, 3), (8, 4, 4, 33), (64, 256, 96, 5)]
+                  (20, 36, 44, 11), (100, 100, 72, 3), (8, 4, 4, 33), (64, 256, 96, 5),
+                  (256, 256, 64, 2), (200, 68, 36, 3), (129, 32, 8, 2)]
 
 
 @pytest.mark.parametrize("m,k,n,npts", GROUPED_SHAPES)
