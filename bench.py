@@ -203,10 +203,10 @@ def tc_ops(cfg):
     if 16 < m <= 32:                       # tc_pq.cu
         nb = pow2(n, 8, 32)
         per = 2 * 128 * 4 * nb * 128 * nch * -(-n // nb)
-    elif 32 < m <= 128 and k % 4 == 0 and n % 4 == 0:   # tc_grouped.cu
+    elif m > 32 and k % 4 == 0 and n % 4 == 0:   # tc_grouped.cu (M-tiled above 128)
         mp = pow2(m, 16, 128)
         nb = pow2(n, 8, min(mp, 64))
-        per = 2 * 128 * 4 * nb * 128 * nch * -(-n // nb)
+        per = 2 * 128 * 4 * nb * 128 * nch * -(-n // nb) * -(-m // 128)
     elif m >= 64 and k % 4 == 0 and 64 <= k <= 8192 and n >= 32:  # tc_pointwise.cu
         per = 2 * 256 * -(-m // 256) * 256 * -(-n // 64) * 128 * nch
     else:

@@ -26,6 +26,7 @@
 // One barrier per column: while updating, the owner of column c+1 of each
 // row already reduces the next pivot key.
 #include <climits>
+#include <cstdlib>
 #include "pmbasis.cuh"
 
 namespace fpm {
@@ -50,15 +51,27 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const F31& f)
   return d_red64((uint64_t)a * b, f.p, f.mu);
 }
 
+// Montgomery product a b 2^-32 mod p (a, b < p)
+__device__ __forceinline__ uint32_t redc_mul(uint32_t a, uint32_t b, const F31& f) {
+  const uint64_t acc = (uint64_t)a * b;
+  const uint32_t m = (uint32_t)acc * f.pinv;
+  const uint32_t t = (uint32_t)((acc + (uint64_t)m * f.p) >> 32);
+  return min(t, t - f.p);
+}
+
+// a^(p-2) by square-and-multiply in the Montgomery domain (cheaper products
+// than Barrett; x -> x 2^32 on entry via r2 = 2^64 mod p, 2^-32 on exit)
 __device__ uint32_t invmod(uint32_t a, const F31& f) {
-  uint32_t r = 1, b = a;
+  const uint32_t r2 = (uint32_t)((((unsigned __int128)1) << 64) % f.p);
+  uint32_t b = redc_mul(a, r2, f);           // a R
+  uint32_t r = redc_mul(1u, r2, f);          // R
   uint32_t e = f.p - 2;
   while (e) {
-    if (e & 1) r = mulmod(r, b, f);
-    b = mulmod(b, b, f);
+    if (e & 1) r = redc_mul(r, b, f);
+    b = redc_mul(b, b, f);
     e >>= 1;
   }
-  return r;
+  return redc_mul(r, 1u, f);                 // out of the Montgomery domain
 }
 
 __device__ __forceinline__ uint64_t fold(uint64_t acc, uint32_t c32) {
@@ -76,9 +89,13 @@ struct StepArgs {
   int64_t* sft_out;   // final shift (m)
   int fold_k;         // products between folds (pointwise.cu fold_period)
   F31 f;
+  unsigned long long* trace;  // profiling only (FPM_MBASIS_TRACE): [T][6] clocks
 };
 
 constexpr int kStepThreads = 512;
+
+#define STEP_TRACE(ev) \
+  if (a.trace && tid == 0) a.trace[k * 8 + (ev)] = clock64();
 
 __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -99,6 +116,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   int* klist = plist + m;                         // m
   __shared__ int s_key[2];
   __shared__ int s_nk;
+  __shared__ uint32_t sbuf[2 * 96];  // block solve: pivot row + column, double buffered
 
   const int hw = tid >> 4, l16 = tid & 15;  // half-warp per row
   constexpr int kRowsPerPass = kStepThreads / 16;
@@ -113,27 +131,146 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   for (int k = 0; k < T; ++k) {
     const uint32_t* Gk = G + (size_t)k * mn;
     for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
-    for (int idx = tid; idx < m * m; idx += kStepThreads)
-      X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
-    for (int i = tid; i < m; i += kStepThreads) {
+    const bool try_fast = m > n && n <= 32 && 2 * n * n + n * (m - n + 1) <= m * m;
+    if (!try_fast)
+      for (int idx = tid; idx < m * m; idx += kStepThreads)
+        X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
+    // rank of row i by (s_i, i): 8 threads per row, shuffle-reduced
+    for (int i0 = 0; i0 < m; i0 += kStepThreads / 8) {
+      const int i = i0 + (tid >> 3), part = tid & 7;
       int r = 0;
-      const int64_t si = sft[i];
-      for (int j = 0; j < m; ++j) r += (sft[j] < si) || (sft[j] == si && j < i);
-      rank[i] = r;
-      ord[r] = i;
-      piv[i] = 0;
+      if (i < m) {
+        const int64_t si = sft[i];
+        for (int j = part; j < m; j += 8) r += (sft[j] < si) || (sft[j] == si && j < i);
+      }
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      r += __shfl_xor_sync(0xffffffffu, r, 4);
+      if (i < m && part == 0) {
+        rank[i] = r;
+        ord[r] = i;
+        piv[i] = 0;
+      }
     }
     if (tid < 2) s_key[tid] = INT_MAX;
     __syncthreads();
+    STEP_TRACE(0);
+
+    // ---- generic residual: block solve ----------------------------------------
+    // When every leading principal minor of R_P (the n lowest-ranked rows,
+    // columns 0..n-1) is nonzero, the column elimination below would pick
+    // exactly those rows as pivots in rank order, and the kernel-row
+    // coefficients are C = R_K R_P^-1 (unique).  Gauss-Jordan on [R_P | I]
+    // with the rows in registers (16 threads x 4 columns per row; one
+    // barrier per column, pivot row / column broadcast through double-
+    // buffered shared memory) plus one dense product give C; a zero leading
+    // minor (degenerate residual) falls back to the general elimination.
+    bool fast_done = false;
+    const int n2 = 2 * n;
+    uint32_t* A = X;                          // [n][2n] after the solve
+    uint32_t* Cs = X + (size_t)n * n2;        // Ct [n][m-n+1] (padded rows)
+    if (try_fast) {
+      const int gi = tid >> 4, gs = tid & 15;  // row gi, columns gs + 16u
+      uint32_t av4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = gs + 16 * u;
+        av4[u] = (gi < n && j < n2)
+                     ? (j < n ? W[(size_t)ord[gi] * n + j] : (j - n == gi ? 1u : 0u))
+                     : 0u;
+      }
+      bool ok = true;
+      for (int c = 0; c < n; ++c) {
+        uint32_t* pb = sbuf + (c & 1) * 96;   // pivot row (64) + pivot column (32)
+        if (gi == c) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pb[gs + 16 * u] = av4[u];
+        }
+        if (gi < n && gs == (c & 15)) pb[64 + gi] = av4[c >> 4];
+        __syncthreads();
+        const uint32_t av = pb[c];
+        if (av == 0) {
+          ok = false;  // uniform: every thread read the same pivot
+          break;
+        }
+        const uint32_t bv = gi < n ? pb[64 + gi] : 0u;
+        if (gi < n && gi != c && bv != 0) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) av4[u] = redc_axby(av, av4[u], bv, pb[gs + 16 * u], f);
+        }
+      }
+      STEP_TRACE(5);
+      if (ok) {
+        if (gi < n) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (gs + 16 * u < n2) A[gi * n2 + gs + 16 * u] = av4[u];
+        }
+        __syncthreads();
+        // R_P^-1 = D^-1 Y: row l of Y scaled by 1 / d_l
+        for (int l = tid; l < n; l += kStepThreads) inv[l] = invmod(A[l * n2 + l], f);
+        // pivots = the n lowest-ranked rows; kernel rows in index order
+        for (int i = tid; i < m; i += kStepThreads) piv[i] = rank[i] < n ? 1 : 0;
+        for (int q = tid; q < n; q += kStepThreads) plist[q] = ord[q];
+        if (tid < 32) {  // warp 0: klist by ballot / popc prefix over the m rows
+          int base = 0;
+          for (int i0 = 0; i0 < m; i0 += 32) {
+            const int i = i0 + tid;
+            const bool kr = i < m && rank[i] >= n;
+            const unsigned bal = __ballot_sync(0xffffffffu, kr);
+            if (kr) klist[base + __popc(bal & ((1u << tid) - 1u))] = i;
+            base += __popc(bal);
+          }
+          if (tid == 0) s_nk = base;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < n * n; idx += kStepThreads) {
+          const int l = idx / n, q = idx - (idx / n) * n;
+          A[l * n2 + n + q] = mulmod(A[l * n2 + n + q], inv[l], f);
+        }
+        __syncthreads();
+        STEP_TRACE(6);
+        // Ct[q][kr] = -(R_K Y')[kr][q]; four independent partial sums (ILP)
+        const int nk = s_nk;
+        // lanes run over q: Y' reads are consecutive, the R_K row is a broadcast
+        for (int idx = tid; idx < n * nk; idx += kStepThreads) {
+          const int kr = idx / n, q = idx - (idx / n) * n;
+          const uint32_t* rk = W + (size_t)klist[kr] * n;
+          uint64_t acc[4] = {0, 0, 0, 0};
+          int cnt = 0;
+          for (int l = 0; l < n; l += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (l + u < n) acc[u] += (uint64_t)rk[l + u] * A[(l + u) * n2 + n + q];
+            if (++cnt == a.fold_k) {
+              cnt = 0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) acc[u] = fold(acc[u], f.c32);
+            }
+          }
+          uint64_t tot = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) tot += d_red64(acc[u], p, f.mu);
+          const uint32_t v = d_red64(tot, p, f.mu);
+          Cs[q * (nk + 1) + kr] = v ? p - v : 0u;  // padded rows: conflict-free stores
+        }
+        fast_done = true;
+      } else {
+        // fallback: the general elimination starts from X = I
+        for (int idx = tid; idx < m * m; idx += kStepThreads)
+          X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
+      }
+      __syncthreads();
+    }
 
     // ---- column elimination, lowest-rank pivot per column --------------------
     // Fast mode: while the pivots so far are exactly ranks 0..np-1, the pivot
     // of column c is the rank-np row if its entry is nonzero (it is then the
     // lowest-ranked candidate) -- no search.  Otherwise (rare: degenerate
     // residuals) switch to the general search for the rest of the step.
-    int np = 0;
+    int np = fast_done ? n : 0;
     bool fastm = true;
-    for (int c = 0; c < n; ++c) {
+    for (int c = 0; c < (fast_done ? 0 : n); ++c) {
       int r = -1;
       if (fastm && np < m) {
         const int rr = ord[np];
@@ -180,32 +317,45 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
       __syncthreads();
     }
 
+    STEP_TRACE(1);
     // ---- record the step; normalise kernel rows: Ct = X_il / X_ii ------------
     if (tid == 0) {
-      int nk = 0;
-      for (int i = 0; i < m; ++i)
-        if (!piv[i]) klist[nk++] = i;
-      s_nk = nk;
+      if (!fast_done) {
+        int nk = 0;
+        for (int i = 0; i < m; ++i)
+          if (!piv[i]) klist[nk++] = i;
+        s_nk = nk;
+      }
       a.rec_np[k] = np;
     }
     for (int q = tid; q < np; q += kStepThreads) a.rec_plist[(size_t)k * m + q] = plist[q];
     __syncthreads();
     const int nk = s_nk;
     if (np == 0) continue;  // R = 0: nothing changes (appint.py:171)
-    for (int kr = tid; kr < nk; kr += kStepThreads) {
-      const int i = klist[kr];
-      inv[kr] = invmod(X[(size_t)i * m + i], f);
-    }
-    __syncthreads();
     uint32_t* Ct = W;  // compact [np][nk]
     uint32_t* recC = a.rec_Ct + (size_t)k * m * m;
-    for (int idx = tid; idx < np * nk; idx += kStepThreads) {
-      const int q = idx / nk, kr = idx - (idx / nk) * nk;
-      const uint32_t v = mulmod(X[(size_t)klist[kr] * m + plist[q]], inv[kr], f);
-      Ct[idx] = v;
-      recC[idx] = v;
+    if (fast_done) {
+      for (int idx = tid; idx < np * nk; idx += kStepThreads) {
+        const int q = idx / nk, kr = idx - (idx / nk) * nk;
+        const uint32_t v = Cs[q * (nk + 1) + kr];
+        Ct[idx] = v;
+        recC[idx] = v;
+      }
+    } else {
+      for (int kr = tid; kr < nk; kr += kStepThreads) {
+        const int i = klist[kr];
+        inv[kr] = invmod(X[(size_t)i * m + i], f);
+      }
+      __syncthreads();
+      for (int idx = tid; idx < np * nk; idx += kStepThreads) {
+        const int q = idx / nk, kr = idx - (idx / nk) * nk;
+        const uint32_t v = mulmod(X[(size_t)klist[kr] * m + plist[q]], inv[kr], f);
+        Ct[idx] = v;
+        recC[idx] = v;
+      }
     }
     __syncthreads();
+    STEP_TRACE(2);
 
     // ---- residual list: kernel rows G[t][i] += sum_q Ct G[t][plist[q]], t > k -
     {
@@ -231,7 +381,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
         }
         if (((n | nk) & 3) == 0 && K == 4) {
           // aligned fast path: 16-byte shared loads, folds at fixed positions
-#pragma unroll 1
+#pragma unroll 4
           for (int q = 0; q < np; ++q) {
             const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + (size_t)plist[q] * n + cb * 4);
             const uint4 c4 = *reinterpret_cast<const uint4*>(Ct + q * nk + rb * 4);
@@ -281,6 +431,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
       }
     }
     __syncthreads();
+    STEP_TRACE(3);
     // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k) ----
     for (int idx = tid; idx < np * n; idx += kStepThreads) {
       const int i = plist[idx / n], j = idx - (idx / n) * n;
@@ -289,6 +440,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     }
     for (int i = tid; i < m; i += kStepThreads) sft[i] += piv[i];
     __syncthreads();
+    STEP_TRACE(4);
   }
   for (int i = tid; i < m; i += kStepThreads) a.sft_out[i] = sft[i];
 }
@@ -374,6 +526,8 @@ __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
   }
 }
 
+unsigned long long* g_step_trace = nullptr;  // FPM_MBASIS_TRACE
+
 F31 make_f31(uint32_t p) {
   F31 f;
   f.p = p;
@@ -424,6 +578,10 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   sa.m = m; sa.n = n; sa.T = order; sa.s = s_dev;
   sa.rec_np = rec_np; sa.rec_plist = rec_plist; sa.rec_Ct = rec_Ct;
   sa.sft_out = sft_dev; sa.fold_k = K; sa.f = f;
+  if (std::getenv("FPM_MBASIS_TRACE")) {
+    if (!g_step_trace) cudaMalloc(&g_step_trace, 64 * 8 * sizeof(unsigned long long));
+    sa.trace = g_step_trace;
+  }
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_steps_kernel,
@@ -454,3 +612,12 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
 }
 
 }  // namespace fpm
+
+// profiling only: per-step phase clocks of the last leaf (FPM_MBASIS_TRACE)
+extern "C" int fpm_debug_mbasis_trace(unsigned long long* host) {
+  if (!fpm::g_step_trace) return 1;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, fpm::g_step_trace, 64 * 8 * sizeof(unsigned long long),
+             cudaMemcpyDeviceToHost);
+  return 0;
+}
