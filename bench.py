@@ -317,8 +317,6 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
     n0 = _lib.launch_count()
     for _ in range(steps):
         flush.zero_()
-        if profile_h is not None:
-            _lib.profile(profile_h, True)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -326,11 +324,17 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
         e1.record()
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-        if profile_h is not None:
+    launches = (_lib.launch_count() - n0) // max(steps, 1) * steps
+    if profile_h is not None:
+        # per-stage CUDA events on separate, untimed steps (the events would
+        # otherwise add to the timed region)
+        for _ in range(min(steps, 3)):
+            flush.zero_()
+            _lib.profile(profile_h, True)
+            run_step(cfg, inputs, out)
+            torch.cuda.synchronize()
             for name, ms in _lib.profile_records(profile_h):
                 stages.setdefault(name, []).append(ms)
-    launches = _lib.launch_count() - n0
-    if profile_h is not None:
         _lib.profile(profile_h, False)
     return times, stages, launches
 
@@ -536,6 +540,8 @@ def main():
     if stages:
         avg = {k: sum(v) / len(v) for k, v in stages.items()}
         line["stages_ms"] = {k: round(v, 5) for k, v in avg.items()}
+        nprof = min(args.steps, 3)
+        line["stages_total_ms_per_step"] = {k: round(sum(v) / nprof, 4) for k, v in stages.items()}
         if cfg["kind"] == "mul":
             line["roofline"], line["roofline_stages"] = roofline_report(cfg, args.config, avg,
                                                                         sbytes)
