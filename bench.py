@@ -80,6 +80,7 @@ def mul_work(cfg):
         "pointwise": r * 4 * N * (m * k + k * n + m * n),
         "ntt_inv": r * m * n * 4 * (N + lc),
     }
+    bytes_["ntt_fwd_AB"] = bytes_["ntt_fwd_A"] + bytes_["ntt_fwd_B"]  # one launch for both
     if r > 1:
         bytes_["crt"] = m * n * lc * (4 * r + 8)
     return modmul, bytes_, N, r
@@ -227,7 +228,11 @@ def roofline_report(cfg, cfgname, avg, sbytes):
     def tr(stage):
         key = "ntt_fwd" if stage.startswith("ntt_fwd") else stage
         v = traffic.get(key)
-        return round(sum(v) / len(v)) if v else None
+        if not v:
+            return None
+        if stage == "ntt_fwd_AB" and len(v) >= 2:
+            return round(sum(v[:2]))  # capture of separate A and B launches
+        return round(sum(v) / len(v))
 
     table = {}
     for st, ms in avg.items():

@@ -380,9 +380,22 @@ int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
 
 }  // namespace
 
-int launch_ntt_fwd(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  if (a.n_entries <= 0) return kOk;
+int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStream_t st) {
   static const bool no_persist = std::getenv("FPM_NTT_NO_PERSIST") != nullptr;
+  if (a_in.n_entries2 > 0) {
+    if (!no_persist && ntt_persist_fwd_ok(logn, a_in) && a_in.n_entries > 0)
+      return launch_ntt_fwd_persist(logn, a_in, ps, st);
+    // generic kernels take one batch at a time
+    NttFwdArgs b1 = a_in, b2 = a_in;
+    b1.n_entries2 = 0;
+    b2.in = a_in.in2; b2.in_stride = a_in.in2_stride; b2.in_prime_stride = a_in.in2_prime_stride;
+    b2.n_entries = a_in.n_entries2; b2.out = a_in.out2; b2.out_prime_stride = a_in.out2_prime_stride;
+    b2.n_entries2 = 0;
+    FPM_TRY(launch_ntt_fwd(logn, b1, ps, st));
+    return launch_ntt_fwd(logn, b2, ps, st);
+  }
+  const NttFwdArgs& a = a_in;
+  if (a.n_entries <= 0) return kOk;
   if (!no_persist && ntt_persist_fwd_ok(logn, a)) return launch_ntt_fwd_persist(logn, a, ps, st);
   switch (logn) {
     case 5: return fwd_impl<5>(a, ps, st);

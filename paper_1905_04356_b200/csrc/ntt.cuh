@@ -39,6 +39,13 @@ struct NttFwdArgs {
   int n_entries;
   uint32_t* out;             // eval layout E[N/32][n_entries][32] (or natural / PM)
   long long out_prime_stride;
+  // optional second batch with the same N, len and flags (persistent kernel
+  // only): one launch for both product operands, no second tail wave
+  const void* in2;
+  long long in2_stride, in2_prime_stride;
+  int n_entries2;            // 0: none
+  uint32_t* out2;
+  long long out2_prime_stride;
 };
 
 struct NttInvArgs {

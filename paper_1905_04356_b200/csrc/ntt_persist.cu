@@ -122,9 +122,13 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   const int tr = G::PAIRED ? (tid & 1) : tid / G::TPT;
   const int lt = G::PAIRED ? (tid >> 1) : tid % G::TPT;
   uint32_t* smt = sm + tr * G::STRIDE;
-  const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
-  const uint32_t* in = (const uint32_t*)a.in + (long long)z * a.in_prime_stride;
-  uint32_t* out = a.out + (long long)z * a.out_prime_stride;
+  const long long groups1 = (a.n_entries + G::TPC - 1) / G::TPC;
+  const long long groups = groups1 + (a.n_entries2 + G::TPC - 1) / G::TPC;
+  const uint32_t* in1 = (const uint32_t*)a.in + (long long)z * a.in_prime_stride;
+  uint32_t* out1 = a.out + (long long)z * a.out_prime_stride;
+  const uint32_t* in2 =
+      a.n_entries2 ? (const uint32_t*)a.in2 + (long long)z * a.in2_prime_stride : in1;
+  uint32_t* out2 = a.n_entries2 ? a.out2 + (long long)z * a.out2_prime_stride : out1;
   const bool upper_zero = G::NPASS > 1 && a.len <= G::N / 2;
   constexpr int FIRST = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
 
@@ -132,10 +136,15 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
 
   uint32_t pre[32];
   auto load_group = [&](long long grp) {
+    const bool second = grp >= groups1;
+    const uint32_t* in = second ? in2 : in1;
+    const long long jn = second ? a.n_entries2 : a.n_entries;
+    const long long jstride = second ? a.in2_stride : a.in_stride;
+    if (second) grp -= groups1;
     if (G::TPT >= 32) {
       const long long e = grp * G::TPC + tr;
-      const bool valid = e < a.n_entries;
-      const uint32_t* src = in + e * a.in_stride;
+      const bool valid = e < jn;
+      const uint32_t* src = in + e * jstride;
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int x = xmap<LOGN, FIRST>(lt, i);
@@ -147,7 +156,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
         const int idx = tid + u * G::THREADS;
         const int t2 = idx >> LOGN, x = idx & (G::N - 1);
         const long long e = grp * G::TPC + t2;
-        pre[u] = (e < a.n_entries && x < a.len) ? __ldg(in + e * a.in_stride + x) : 0u;
+        pre[u] = (e < jn && x < a.len) ? __ldg(in + e * jstride + x) : 0u;
       }
     }
   };
@@ -173,32 +182,35 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     constexpr bool kPrefetch = G::THREADS <= 512;  // 32 extra registers
     if (kPrefetch && nxt < groups) load_group(nxt);  // in flight during the passes
     fwd_passes<LOGN, TPCX>(v, smt, tws, pc, lt, upper_zero);
-    const long long e0 = grp * G::TPC, e = e0 + tr;
+    const bool second = grp >= groups1;
+    uint32_t* out = second ? out2 : out1;
+    const long long jn = second ? a.n_entries2 : a.n_entries;
+    const long long e0 = (second ? grp - groups1 : grp) * G::TPC, e = e0 + tr;
     if (G::PAIRED && a.pm) {
       // lane pair (tr = 0, 1) holds the two transforms of the same 32 points:
       // exchange half of them so each lane writes (T0[x], T1[x]) as 8 bytes
-      const bool vec = (a.n_entries & 1) == 0 && e0 + 1 < a.n_entries;
+      const bool vec = (jn & 1) == 0 && e0 + 1 < jn;
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const uint32_t send = tr ? v[i] : v[i + 1];
         const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
         const int x = xmap<LOGN, MAP_LAST>(lt, i + tr);
         const uint32_t lo = tr ? recv : v[i], hi = tr ? v[i + 1] : recv;
-        uint32_t* dst = out + (long long)x * a.n_entries + e0;
+        uint32_t* dst = out + (long long)x * jn + e0;
         if (vec) {
           *reinterpret_cast<uint2*>(dst) = make_uint2(lo, hi);
         } else {
-          if (e0 < a.n_entries) dst[0] = lo;
-          if (e0 + 1 < a.n_entries) dst[1] = hi;
+          if (e0 < jn) dst[0] = lo;
+          if (e0 + 1 < jn) dst[1] = hi;
         }
       }
     } else if (G::TPC == 1 && a.pm) {
       // point-major scatter straight from registers (4-byte pieces; the
       // other entries of each 32-byte sector come from neighbouring CTAs)
-      if (e < a.n_entries) {
+      if (e < jn) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
-          out[(long long)xmap<LOGN, MAP_LAST>(lt, i) * a.n_entries + e] = v[i];
+          out[(long long)xmap<LOGN, MAP_LAST>(lt, i) * jn + e] = v[i];
       }
     } else if (a.pm) {
       __syncthreads();
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
       __syncthreads();
       constexpr int PW = G::TPC < 4 ? G::TPC : 4;  // values per row piece
       constexpr int GQ = G::TPC / PW;
-      const bool vec = (a.n_entries % PW) == 0;
+      const bool vec = (jn % PW) == 0;
 #pragma unroll 8
       for (int idx = tid; idx < G::N * GQ; idx += G::THREADS) {
         const int x = idx / GQ, gq = idx - (idx / GQ) * GQ;
@@ -214,8 +226,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
         uint32_t w[PW];
 #pragma unroll
         for (int q = 0; q < PW; ++q) w[q] = sm[(PW * gq + q) * G::STRIDE + pad(x)];
-        uint32_t* dst = out + (long long)x * a.n_entries + eb;
-        if (vec && eb + PW - 1 < a.n_entries) {
+        uint32_t* dst = out + (long long)x * jn + eb;
+        if (vec && eb + PW - 1 < jn) {
           if constexpr (PW == 4)
             *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
           else
@@ -223,14 +235,14 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
         } else {
 #pragma unroll
           for (int q = 0; q < PW; ++q)
-            if (eb + q < a.n_entries) dst[q] = w[q];
+            if (eb + q < jn) dst[q] = w[q];
         }
       }
-    } else if (e < a.n_entries) {
+    } else if (e < jn) {
       const int pl = a.pblk_log ? a.pblk_log : 5;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<uint4*>(out + eval_piece(lt * 32 + 4 * q, e, a.n_entries, pl)) =
+        *reinterpret_cast<uint4*>(out + eval_piece(lt * 32 + 4 * q, e, jn, pl)) =
             make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     }
     __syncthreads();  // smem exchange buffer reused by the next group
@@ -416,7 +428,8 @@ int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
   }
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
+  long long groups = (a.n_entries + G::TPC - 1) / G::TPC;
+  if constexpr (FWD) groups += (a.n_entries2 + G::TPC - 1) / G::TPC;
   long long grid = (long long)blocks_per_sm * sms / ps.count;
   if (grid < 1) grid = 1;
   if (grid > groups) grid = groups;

@@ -169,16 +169,26 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   fa.natural = 0; fa.pm = use_tc; fa.pblk_log = pq ? 2 : 5;
   fa.n_entries = (int)ea; fa.out = EA; fa.out_prime_stride = N * ea;
   if (direct && A.is64) fa.reduce = 0;
-  {
-    StageTimer t_(cx, "ntt_fwd_A");
-    FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
-  }
   NttFwdArgs fb = fa;
   fb.in = B.ptr; fb.in64 = B.is64; fb.in_stride = B.stride; fb.len = B.len; fb.fold = fold;
   fb.reduce = reduce_needed || (!direct && B.is64);
   if (direct && B.is64) fb.reduce = 0;
   fb.n_entries = (int)eb; fb.out = EB; fb.out_prime_stride = N * eb;
-  {
+  // both operands in one launch when their transforms are alike (persistent
+  // grid: one tail wave instead of two)
+  static const bool no_pair = std::getenv("FPM_NTT_NO_PAIR") != nullptr;
+  if (!no_pair && fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
+      fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
+    NttFwdArgs fab = fa;
+    fab.in2 = fb.in; fab.in2_stride = fb.in_stride; fab.in2_prime_stride = fb.in_prime_stride;
+    fab.n_entries2 = fb.n_entries; fab.out2 = fb.out; fab.out2_prime_stride = fb.out_prime_stride;
+    StageTimer t_(cx, "ntt_fwd_AB");
+    FPM_TRY(launch_ntt_fwd(logn, fab, ps, st));
+  } else {
+    {
+      StageTimer t_(cx, "ntt_fwd_A");
+      FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
+    }
     StageTimer t_(cx, "ntt_fwd_B");
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
   }
