@@ -40,15 +40,24 @@ __device__ __forceinline__ void row_apply_s(uint32_t (&v)[32], const uint2* tws,
   }
 }
 
+// asynchronous copy of the twiddle table into shared memory (cp.async: all
+// pieces in flight at once, no register round trip); the caller's
+// __syncthreads() after cp_async_wait_all() publishes it
 template <int LOGN>
 __device__ __forceinline__ void stage_table(uint2* tws, const uint2* __restrict__ tw) {
   constexpr int N = 1 << LOGN;
   // N entries = N/32 rows x 16 pairs
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(tws);
   for (int idx = threadIdx.x; idx < N / 2; idx += blockDim.x) {
     const int r = idx >> 4, q = idx & 15;
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(tw) + idx);
-    reinterpret_cast<uint4*>(tws)[r * 16 + (q ^ sw_row(r))] = v;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(
+                     base + 16u * (uint32_t)(r * 16 + (q ^ sw_row(r)))),
+                 "l"(reinterpret_cast<const uint4*>(tw) + idx));
   }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 template <int LOGN, int TPCX>
@@ -163,6 +172,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
 
   long long grp = blockIdx.x;
   if (grp < groups) load_group(grp);
+  cp_async_wait_all();
   __syncthreads();  // table staged
   for (; grp < groups; grp += gridDim.x) {
     uint32_t v[32];
@@ -339,7 +349,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
 
   long long grp = blockIdx.x;
   if (grp < groups) load_group(grp);
-  __syncthreads();
+  cp_async_wait_all();
+  __syncthreads();  // table staged
   for (; grp < groups; grp += gridDim.x) {
     uint32_t v[32];
     if (G::PAIRED && a.pm) {

@@ -152,8 +152,17 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // point-quad TC kernel for 16 < m <= 32 (cfg2: 0.205 vs 0.225 ms on the
   // CUDA cores); m <= 16 stays on the CUDA cores (cfg3: 35 vs 75 us)
   static const bool pq_off = std::getenv("FPM_DISABLE_TC_PQ") != nullptr;
-  bool pq = !tc_off && !pq_off && logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
-  for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
+  // limbs-on-M variant (tc_pq2.cu): exact and TMEM-light, but its shuffle
+  // reduce-scatter epilogue costs more than it saves on cfg2 (49.5 vs 45 us);
+  // opt-in until that epilogue is cheaper
+  static const bool pq2_on = std::getenv("FPM_ENABLE_TC_PQ2") != nullptr;
+  bool pq2 = !tc_off && pq2_on && logn <= 13 && (long long)m * k * n >= 4096;
+  for (int i = 0; i < r && pq2; ++i) pq2 = tc_pq2_applicable(m, k, n, (int)N, primes[i]);
+  bool pq = pq2;
+  if (!pq2) {
+    pq = !tc_off && !pq_off && logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
+    for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
+  }
   // grouped / M-tiled PM-layout TC kernel (TMA, warp specialised) for m > 32;
   // tc_pointwise.cu remains for shapes it does not take (p < 2^30)
   bool grouped = !pq && !tc_off && !small_off && logn <= 13 && m > 32 &&
@@ -198,7 +207,10 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
     ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
     StageTimer t_(cx, "pointwise_tc");
-    FPM_TRY(launch_tc_pq(ta, ps, st));
+    if (pq2)
+      FPM_TRY(launch_tc_pq2(ta, ps, st));
+    else
+      FPM_TRY(launch_tc_pq(ta, ps, st));
   } else if (use_tc) {
     TcArgs ta{};
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;

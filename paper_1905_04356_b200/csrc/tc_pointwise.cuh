@@ -25,4 +25,8 @@ int launch_tc_grouped(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 bool tc_pq_applicable(int m, int k, int n, int npts, uint32_t p);
 int launch_tc_pq(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// m, n <= 32 on the point-quad layout, limbs on M (tc_pq2.cu)
+bool tc_pq2_applicable(int m, int k, int n, int npts, uint32_t p);
+int launch_tc_pq2(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 }  // namespace fpm

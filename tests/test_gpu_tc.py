@@ -114,17 +114,21 @@ PQ_SHAPES = [(32, 32, 32, 16), (16, 16, 16, 24), (17, 5, 9, 8), (1, 1, 1, 8), (3
              (24, 100, 40, 16), (8, 4, 4, 32), (32, 33, 70, 8)]
 
 
+@pytest.mark.parametrize("kernel", ["fpm_selftest_tc_pq", "fpm_selftest_tc_pq2"])
 @pytest.mark.parametrize("m,k,n,npts", PQ_SHAPES)
-def test_tc_pq_exact(m, k, n, npts):
+def test_tc_pq_exact(m, k, n, npts, kernel):
     """Point-quad kernel: k / n tails, m not a power of two, several n-blocks,
     three primes, a point of all p-1 (largest limb sums)."""
     import numpy as np
 
     primes = [2013265921, 2130706433, 1107296257]
     L = _lib.lib()
-    L.fpm_selftest_tc_pq.restype = ctypes.c_int
-    L.fpm_selftest_tc_pq.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int] + \
+    fn = getattr(L, kernel)
+    fn.restype = ctypes.c_int
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int] + \
         [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
+    if kernel.endswith("pq2") and n > 32:
+        pytest.skip("tc_pq2 takes n <= 32")
     h = _lib.context()
     rng = np.random.default_rng(11 * m + 5 * k + n + npts)
     A = np.stack([rng.integers(0, q, size=(npts, m, k), dtype=np.uint64) for q in primes])
@@ -136,8 +140,8 @@ def test_tc_pq_exact(m, k, n, npts):
     Bd = torch.from_numpy(_to_pq(B).astype(np.uint32).view(np.int32)).cuda()
     Cd = torch.full((len(primes), npts // 4, m, n, 4), -1, dtype=torch.int32, device="cuda")
     pr = (ctypes.c_uint32 * len(primes))(*primes)
-    _lib.check(L.fpm_selftest_tc_pq(h, pr, len(primes), Ad.data_ptr(), Bd.data_ptr(),
-                                    Cd.data_ptr(), m, k, n, npts), "tc_pq")
+    _lib.check(fn(h, pr, len(primes), Ad.data_ptr(), Bd.data_ptr(), Cd.data_ptr(), m, k, n,
+                  npts), kernel)
     C = _from_pq(Cd.cpu().numpy().view(np.uint32).astype(np.uint64))
     for z, q in enumerate(primes):
         for t in range(npts):

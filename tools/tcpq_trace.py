@@ -24,9 +24,10 @@ def main():
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 512)()
     L = _lib.lib()
-    assert L.fpm_debug_tcpq_trace(buf) == 0
+    fn = L.fpm_debug_tcpq2_trace if os.environ.get("FPM_TCPQ2_TRACE") else L.fpm_debug_tcpq_trace
+    assert fn(buf) == 0
     t0 = buf[0]
-    names = ["tma", "A_full", "A_done", "B_full", "B_done", "mma", "epi_t", "epi_done"]
+    names = (["tma", "A_full", "A_done", "B_done", "mma", "epi_t", "epi_stg", "epi_done"] if os.environ.get("FPM_TCPQ2_TRACE") else ["tma", "A_full", "A_done", "B_full", "B_done", "mma", "epi_t", "epi_done"])
     print("item " + " ".join(f"{n:>9s}" for n in names))
     for i in range(20):
         row = [buf[i * 8 + e] for e in range(8)]
