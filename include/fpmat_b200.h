@@ -94,6 +94,19 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes,
                         const void* A_host, int m, int k, int la,
                         const void* B_host, int n, int lb, void* C_host);
 
+/* ---- Multiplier (polmat.Multiplier / multiplier_precompute /
+ *      multiplier_apply, polmat.py:550-610) ------------------------------------
+ * A fixed left factor A (m x k, length la; copied on create) whose forward
+ * transforms stay cached on the device: each apply transforms only B.
+ * max_rhs_len = max_rhs_degree + 1 fixes the cyclic length; an apply with
+ * lb > max_rhs_len returns FPM_ERR_ENVELOPE_EXCEEDED (polmat.py:583-586).
+ * C_dev receives m x n with length la + lb - 1. */
+typedef struct fpm_multiplier fpm_multiplier;
+int fpm_multiplier_create(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A_dev,
+                          int m, int k, int la, int max_rhs_len, fpm_multiplier** out);
+int fpm_multiplier_apply(fpm_multiplier* mult, const void* B_dev, int n, int lb, void* C_dev);
+void fpm_multiplier_destroy(fpm_multiplier* mult);
+
 /* ---- middle product (polmat._pm_middle / pm_middle_product,
  *      polmat.py:470-536) ----------------------------------------------------
  * R (m x n, length d): exact == 0 reproduces the reference `_pm_middle`

@@ -87,6 +87,10 @@ def lib():
             "fpm_pmbasis_host": (i32, [vp, u64, i32, vp, i32, i32, i32, i32, pi64, vp, pint,
                                        pi64]),
             "fpm_set_pmbasis_threshold": (i32, [vp, i32]),
+            "fpm_multiplier_create": (i32, [vp, u64, i32, vp, i32, i32, i32, i32,
+                                            ctypes.POINTER(vp)]),
+            "fpm_multiplier_apply": (i32, [vp, vp, i32, i32, vp]),
+            "fpm_multiplier_destroy": (None, [vp]),
             "fpm_profile_enable": (i32, [vp, i32]),
             "fpm_profile_count": (i32, [vp]),
             "fpm_profile_get": (i32, [vp, i32, ctypes.c_char_p, i32,

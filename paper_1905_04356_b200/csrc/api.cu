@@ -193,6 +193,79 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   return kOk;
 }
 
+struct fpm_multiplier {
+  fpm_context* ctx;
+  uint64_t p;
+  int elem_bytes, m, k, la, max_rhs_len, logn;
+  void* A;  // device copy of the left factor
+  fpm::EvalCache cache;
+};
+
+int fpm_multiplier_create(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
+                          int k, int la, int max_rhs_len, fpm_multiplier** out) {
+  using namespace fpm;
+  if (!ctx || !out) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  FPM_TRY(check_dims(m, k, 0));
+  if (la < 0 || max_rhs_len < 1) {
+    set_last_error("multiplier: la = %d, max_rhs_len = %d", la, max_rhs_len);
+    return kInvalidArgument;
+  }
+  Context& cx = *ctx->cx;
+  auto* mu = new fpm_multiplier();
+  mu->ctx = ctx; mu->p = p; mu->elem_bytes = elem_bytes; mu->m = m; mu->k = k; mu->la = la;
+  mu->max_rhs_len = max_rhs_len;
+  mu->logn = ceil_log2_min1((long long)(la > 0 ? la : 1) + max_rhs_len - 1);
+  const size_t bytes = (size_t)elem_bytes * m * k * (la > 0 ? la : 0);
+  mu->A = nullptr;
+  if (bytes) {
+    const int s = cx.alloc(bytes, &mu->A);
+    if (s != kOk) {
+      delete mu;
+      return s;
+    }
+    const cudaError_t e = cudaMemcpyAsync(mu->A, A, bytes, cudaMemcpyDeviceToDevice, cx.stream());
+    if (e != cudaSuccess) {
+      cx.release(mu->A);
+      delete mu;
+      set_last_error("multiplier: copy of A failed (%s)", cudaGetErrorString(e));
+      return kCudaError;
+    }
+  }
+  *out = mu;
+  return kOk;
+}
+
+int fpm_multiplier_apply(fpm_multiplier* mu, const void* B, int n, int lb, void* C) {
+  using namespace fpm;
+  if (!mu) return kInvalidArgument;
+  FPM_TRY(check_dims(mu->m, mu->k, n));
+  if (lb > mu->max_rhs_len) {
+    set_last_error("deg B = %d exceeds the multiplier envelope %d", lb - 1,
+                   mu->max_rhs_len - 1);
+    return kEnvelopeExceeded;
+  }
+  Context& cx = *mu->ctx->cx;
+  const int is64 = mu->elem_bytes == 8;
+  const int la = mu->la;
+  const int lc = (la > 0 && lb > 0) ? la + lb - 1 : 0;
+  OutRef Cr{C, is64, lc, lc};
+  if (la <= 0 || lb <= 0 || mu->k == 0)
+    return polmat_mul(cx, mu->p, mu->m, mu->k, n, MatRef{mu->A, is64, la, la},
+                      MatRef{B, is64, lb, lb}, Cr);
+  return cyclic_product(cx, mu->p, mu->m, mu->k, n, MatRef{mu->A, is64, la, la},
+                        MatRef{B, is64, lb, lb}, mu->logn, 0, Cr, &mu->cache);
+}
+
+void fpm_multiplier_destroy(fpm_multiplier* mu) {
+  if (!mu) return;
+  fpm::Context& cx = *mu->ctx->cx;
+  cudaStreamSynchronize(cx.stream());
+  if (mu->A) cx.release(mu->A);
+  if (mu->cache.EA) cx.release(mu->cache.EA);
+  delete mu;
+}
+
 int fpm_polmat_middle(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
                       int k, int la, const void* B, int n, int lb, long long c, int d, int exact,
                       void* R) {

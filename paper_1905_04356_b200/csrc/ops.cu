@@ -87,7 +87,7 @@ int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L
 }
 
 int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
-                   int logn, long long off, OutRef C) {
+                   int logn, long long off, OutRef C, EvalCache* cache) {
   cudaStream_t st = cx.stream();
   const long long ec = (long long)m * n;
   if (ec == 0 || C.len <= 0) return kOk;
@@ -139,8 +139,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // ---- workspaces ------------------------------------------------------------
   Workspace ws(cx);
   const long long ea = (long long)m * k, eb = (long long)k * n;
-  uint32_t *EA, *EB, *EC;
-  FPM_TRY(ws.get(r * N * ea, &EA));
+  uint32_t *EA = nullptr, *EB, *EC;
+  if (!cache) FPM_TRY(ws.get(r * N * ea, &EA));
   FPM_TRY(ws.get(r * N * eb, &EB));
   FPM_TRY(ws.get(r * N * ec, &EC));
 
@@ -183,11 +183,42 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   fb.reduce = reduce_needed || (!direct && B.is64);
   if (direct && B.is64) fb.reduce = 0;
   fb.n_entries = (int)eb; fb.out = EB; fb.out_prime_stride = N * eb;
+  bool a_cached = false;
+  if (cache) {
+    const int pm_now = use_tc ? 1 : 0, pl_now = pq ? 2 : 5;
+    bool match = cache->valid && cache->p == p && cache->m == m && cache->k == k &&
+                 cache->a_len == A.len && cache->logn == logn && cache->r == r &&
+                 cache->pm == pm_now && cache->pblk_log == pl_now;
+    for (int i = 0; i < r && match; ++i) match = cache->primes[i] == primes[i];
+    const size_t words = (size_t)r * N * ea;
+    if (!match) {
+      if (cache->EA && cache->words < words) {
+        cx.release(cache->EA);
+        cache->EA = nullptr;
+      }
+      if (!cache->EA) {
+        void* ptr = nullptr;
+        FPM_TRY(cx.alloc(words * 4, &ptr));
+        cache->EA = (uint32_t*)ptr;
+        cache->words = words;
+      }
+      cache->valid = false;
+      cache->p = p; cache->m = m; cache->k = k; cache->a_len = A.len; cache->logn = logn;
+      cache->r = r; cache->pm = pm_now; cache->pblk_log = pl_now;
+      for (int i = 0; i < r; ++i) cache->primes[i] = primes[i];
+    }
+    EA = cache->EA;
+    fa.out = EA;
+    a_cached = match;
+  }
   // both operands in one launch when their transforms are alike (persistent
   // grid: one tail wave instead of two)
   static const bool no_pair = std::getenv("FPM_NTT_NO_PAIR") != nullptr;
-  if (!no_pair && fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
-      fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
+  if (a_cached) {
+    StageTimer t_(cx, "ntt_fwd_B");
+    FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
+  } else if (!no_pair && fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
+             fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
     NttFwdArgs fab = fa;
     fab.in2 = fb.in; fab.in2_stride = fb.in_stride; fab.in2_prime_stride = fb.in_prime_stride;
     fab.n_entries2 = fb.n_entries; fab.out2 = fb.out; fab.out2_prime_stride = fb.out_prime_stride;
@@ -201,6 +232,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     StageTimer t_(cx, "ntt_fwd_B");
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
   }
+
+  if (cache) cache->valid = true;  // A's evaluations are in place (stream order)
 
   if (pq) {
     TcArgs ta{};

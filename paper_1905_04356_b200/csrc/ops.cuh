@@ -26,11 +26,24 @@ struct OutRef {
   int len;  // coefficients written per entry
 };
 
+// cached evaluations of a fixed left factor (Multiplier, polmat.py:550-610):
+// valid for one (p, m, k, len(A), N, prime set, eval layout); refreshed in
+// place when a product needs another layout
+struct EvalCache {
+  bool valid = false;
+  uint64_t p = 0;
+  int m = 0, k = 0, a_len = 0, logn = 0, r = 0, pm = 0, pblk_log = 0;
+  uint32_t primes[kMaxPrimes] = {};
+  uint32_t* EA = nullptr;  // context allocation, r * N * m * k words
+  size_t words = 0;
+};
+
 // C = window of (A * fold_N(B)) mod (x^N - 1) over F_p:
 //   C[e][t] = cyc[(off + t) mod N], t < out.len, N = 2^logn.
 // With N >= len(A) + len(B) - 1 and no fold this is the plain product.
+// With `cache`, A's forward transforms are taken from / stored into it.
 int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
-                   int logn, long long off, OutRef C);
+                   int logn, long long off, OutRef C, EvalCache* cache = nullptr);
 
 // full product A*B (length la + lb - 1, truncated/padded to C.len)
 int polmat_mul(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B, OutRef C);

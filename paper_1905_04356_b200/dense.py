@@ -164,3 +164,49 @@ def ntt_dense(x, p, log_len, inverse=False):
     _lib.check(L.fpm_ntt_u64(h, p, log_len, batch, x64.data_ptr(), out.data_ptr(),
                              1 if inverse else 0), "fpm_ntt_u64")
     return out.to(x.dtype) if x.dtype != torch.int64 else out
+
+
+class DenseMultiplier:
+    """Fixed left factor on the device with cached forward transforms
+    (fpm_multiplier_*; reference polmat.Multiplier, polmat.py:550-610)."""
+
+    def __init__(self, A, p, max_rhs_len):
+        _check_tensor(A, p, "A")
+        self.p = p
+        self.m, self.k, self.la = A.shape
+        self.max_rhs_len = int(max_rhs_len)
+        self._h = _lib.context(A.device.index)
+        self._mu = ctypes.c_void_p()
+        _lib.check(_lib.lib().fpm_multiplier_create(self._h, p, elem_bytes_for(p), A.data_ptr(),
+                                                     self.m, self.k, self.la, self.max_rhs_len,
+                                                     ctypes.byref(self._mu)),
+                   "fpm_multiplier_create")
+        self.device = A.device
+        self.dtype = A.dtype
+
+    def apply(self, B, out=None):
+        import torch
+
+        _check_tensor(B, self.p, "B")
+        k2, n, lb = B.shape
+        if k2 != self.k:
+            from .errors import DimMismatch
+
+            raise DimMismatch(f"cannot multiply {self.m}x{self.k} by {k2}x{n}")
+        lc = self.la + lb - 1 if self.la > 0 and lb > 0 else 0
+        if out is None:
+            out = torch.empty((self.m, n, lc), dtype=self.dtype, device=self.device)
+        _lib.check(_lib.lib().fpm_multiplier_apply(self._mu, B.data_ptr(), n, lb, out.data_ptr()),
+                   "fpm_multiplier_apply")
+        return out
+
+    def close(self):
+        if self._mu:
+            _lib.lib().fpm_multiplier_destroy(self._mu)
+            self._mu = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

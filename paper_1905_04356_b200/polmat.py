@@ -293,9 +293,11 @@ class Multiplier:
             return PolMat.zeros(A.ctx, A.m, B.n)
         p = A.ctx.p
         if self._dev is None:
-            self._dev = dense.to_device(to_dense(A), p)
+            # A's forward transforms are computed once and cached on the device
+            self._dev = dense.DenseMultiplier(dense.to_device(to_dense(A), p), p,
+                                              self.max_rhs_degree + 1)
         b = dense.to_device(to_dense(B), p)
-        c = dense.pm_mul_dense(self._dev, b, p)
+        c = self._dev.apply(b)
         return from_dense(A.ctx, dense.to_numpy(c, p), ncols=B.n)
 
 

@@ -120,6 +120,39 @@ def test_pm_mul_vs_oracle(p, m, k, n, la, lb):
     assert np.array_equal(C.astype(np.uint64), O.pm_mul(p, A, B))
 
 
+@pytest.mark.parametrize("p,m,k,la,env", [
+    (P31, 32, 32, 1000, 1500),      # point-quad tensor-core layout cached
+    (P31, 4, 3, 300, 300),          # CUDA-core blocked layout
+    (P31, 72, 64, 100, 200),        # point-major (grouped TC) layout
+    (P60, 5, 4, 200, 250),          # multi-prime: cache keyed by the prime set
+    (97, 3, 3, 10, 12),             # tiny two-adicity
+])
+def test_multiplier_cached_evaluations(p, m, k, la, env):
+    """Multiplier (polmat.py:550-610): A's transforms cached on the device; every
+    apply equals the product, layouts switch when n changes the kernel choice."""
+    A = _dense_rand(p, (m, k, la), 31 + m)
+    mu = dense.DenseMultiplier(dense.to_device(A, p), p, env)
+    for idx, (n, lb) in enumerate([(m, env), (3, env // 2), (m, 1), (40, env)]):
+        B = _dense_rand(p, (k, n, lb), 50 + idx)
+        C = dense.to_numpy(mu.apply(dense.to_device(B, p)), p)
+        assert np.array_equal(C.astype(np.uint64), O.pm_mul(p, A, B)), (n, lb)
+    with pytest.raises(F.errors.EnvelopeExceeded):
+        mu.apply(dense.to_device(_dense_rand(p, (k, 2, env + 1), 9), p))
+    mu.close()
+
+
+def test_multiplier_polmat_api():
+    ctx = F.field_new(P31)
+    rng = random.Random(4)
+    A = F.random_polmat(ctx, 3, 4, 40, rng)
+    mu = F.polmat.multiplier_precompute(A, 60)
+    for d in (60, 10, 0):
+        B = F.random_polmat(ctx, 4, 2, d, rng)
+        assert F.polmat.multiplier_apply(mu, B) == F.pm_mul(A, B)
+    with pytest.raises(F.errors.EnvelopeExceeded):
+        F.polmat.multiplier_apply(mu, F.random_polmat(ctx, 4, 2, 61, rng))
+
+
 def test_host_abi_matches_device():
     import ctypes
 
