@@ -21,6 +21,7 @@ from .polmat import (  # noqa: F401
     random_polmat,
 )
 from .appint import mbasis, mbasis1, pmbasis  # noqa: F401
+from . import fraction, kernel  # noqa: F401,E402  (callers one level up)
 
 __all__ = [
     "FieldCtx", "NttPlan", "field_new", "cached_field", "ntt_forward", "ntt_inverse",

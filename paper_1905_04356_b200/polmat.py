@@ -134,6 +134,34 @@ class PolMat:
     def is_zero(self):
         return all(not e for row in self.rows for e in row)
 
+    # ---- entrywise arithmetic (host; polmat.py:199-231) ----------------------
+    def _entrywise(self, other, sign):
+        _same_ctx(self, other)
+        if (self.m, self.n) != (other.m, other.n):
+            raise DimMismatch(f"shapes {self.m}x{self.n} and {other.m}x{other.n} differ")
+        p = self.ctx.p
+
+        def comb(a, b):
+            L = max(len(a), len(b))
+            a = a + [0] * (L - len(a))
+            b = b + [0] * (L - len(b))
+            return _trim([(x + sign * y) % p for x, y in zip(a, b)])
+
+        return PolMat(self.ctx, [[comb(a, b) for a, b in zip(ra, rb)]
+                                 for ra, rb in zip(self.rows, other.rows)], ncols=self.n)
+
+    def __add__(self, other):
+        return self._entrywise(other, 1)
+
+    def __sub__(self, other):
+        return self._entrywise(other, -1)
+
+    def scale(self, c):
+        p = self.ctx.p
+        c %= p
+        return PolMat(self.ctx, [[_trim([x * c % p for x in e]) for e in row]
+                                 for row in self.rows], ncols=self.n)
+
     def __eq__(self, other):
         # duck-typed so reference PolMat values compare equal (polmat.py:184-189)
         return (hasattr(other, "rows") and hasattr(other, "ctx")

@@ -157,3 +157,22 @@ def test_bridge_rebinds_and_restores(tmp_path, monkeypatch):
     assert app._pm_middle is not saved[("fakefpmat.appint", "_pm_middle")]
     uninstall(saved)
     assert kern.pm_mul(None, None) == "ref" and app.pmbasis(None, 1, [0]) == "ref"
+
+
+def test_polmat_entrywise_arithmetic():
+    ctx = F.field_new(97)
+    A = F.PolMat(ctx, [[[1, 96], [5]], [[], [3, 4, 90]]])
+    B = F.PolMat(ctx, [[[96, 1], []], [[2], [94, 93, 7]]])
+    assert (A + B).rows == [[[], [5]], [[2], []]]  # 3+94, 4+93, 90+7 = 0 mod 97
+    assert (A - A).is_zero()
+    assert (A + B - B) == A
+    assert A.scale(-1) == F.PolMat.zeros(ctx, 2, 2) - A
+    assert (A + B).rows[0][0] == []  # 1+96 = 0, 96+1 = 0 -> trimmed
+
+
+def test_caller_goldens_present():
+    import json
+    import os
+
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "callers.json")))
+    assert len(d["fracrec"]) >= 10 and len(d["kernel"]) >= 6
