@@ -11,6 +11,8 @@
 //     in an m x m transform matrix X (basis row i = X[i]);
 //   * P <- Q P with pivot rows shifted by x (appint.py:79-117), trailing
 //     zero coefficient matrices popped, s <- rdeg_s(P) (appint.py:179).
+#include <cstdlib>
+
 #include "pmbasis.cuh"
 #include <algorithm>
 #include <climits>
@@ -392,6 +394,39 @@ int pmbasis_rec(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
   return kOk;
 }
 
+// Sync-free recursion for 31-bit primes with shared-memory leaves: the
+// shift stays on the device (each leaf turns s into s + delta, which equals
+// rdeg_s of its basis, and composing leaves composes the shifts), and all
+// lengths use the a-priori bound deg P <= order, so no node waits for the
+// host.  Inside PM-Basis P1 F = 0 mod x^o1, so the reference's _pm_middle
+// equals the true slice (exact = 1) whatever the cyclic length.
+int pmbasis_rec_dev(Context& cx, uint32_t p, const void* F, int m, int n, long long fs, int lf,
+                    int order, const int64_t* s_dev, int T, void* P, long long ps,
+                    int64_t* sft_dev) {
+  const int lt = lf < order ? lf : order;
+  if (order <= T) return mbasis_fast(cx, p, F, m, n, fs, lt, order, s_dev, P, ps, sft_dev);
+  const int o1 = (order + 1) / 2, o2 = order - o1;
+  Workspace ws(cx);
+  uint32_t *P1, *R, *P2;
+  int64_t* s1;
+  FPM_TRY(ws.get((size_t)m * m * (o1 + 1), &P1));
+  FPM_TRY(ws.get((size_t)m, &s1));
+  FPM_TRY(pmbasis_rec_dev(cx, p, F, m, n, fs, lf < o1 ? lf : o1, o1, s_dev, T, P1, o1 + 1, s1));
+  FPM_TRY(ws.get((size_t)m * n * (o2 > 0 ? o2 : 1), &R));
+  {
+    MatRef A{P1, 0, o1 + 1, o1 + 1};
+    MatRef B{F, 0, fs, lt};
+    OutRef Ro{R, 0, o2, o2};
+    FPM_TRY(polmat_middle(cx, p, m, m, n, A, B, o1, lt - 1, o1, o2, 1, Ro));
+  }
+  FPM_TRY(ws.get((size_t)m * m * (o2 + 1), &P2));
+  FPM_TRY(pmbasis_rec_dev(cx, p, R, m, n, o2, o2, o2, s1, T, P2, o2 + 1, sft_dev));
+  MatRef A2{P2, 0, o2 + 1, o2 + 1};
+  MatRef B2{P1, 0, o1 + 1, o1 + 1};
+  OutRef Co{P, 0, ps, (int)ps};
+  return polmat_mul(cx, p, m, m, m, A2, B2, Co);
+}
+
 }  // namespace
 
 int mbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, long long fs,
@@ -416,10 +451,31 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
   // the output does not depend on T (product of canonical steps): cap it so
   // leaves run on the shared-memory M-Basis kernels when they apply
   if (!is64 && p < (1ull << 31)) {
+    // shared-memory leaves; order 8 balances the per-step residual-list
+    // update (grows with the leaf order) against the tree's products
+    // (cfg4: T = 16 179 ms, T = 8 168 ms, T = 4 184 ms)
     const int tf = mbasis_fast_max_order(m, n);
-    if (tf >= 1 && T > tf) T = tf;
+    const int tcap = tf < 8 ? tf : 8;
+    if (tf >= 1 && T > tcap) T = tcap;
   }
   std::vector<int64_t> s(shift, shift + m);
+  static const bool dev_off = std::getenv("FPM_PMBASIS_HOST_SYNC") != nullptr;
+  if (!dev_off && !is64 && p < (1ull << 31) && m > 0 && order >= 1 && T >= 1 &&
+      T <= mbasis_fast_max_order(m, n) && ps >= order + 1) {
+    Workspace ws(cx);
+    int64_t *s_dev, *sft_dev;
+    FPM_TRY(ws.get((size_t)m, &s_dev));
+    FPM_TRY(ws.get((size_t)m, &sft_dev));
+    FPM_CUDA_TRY(cudaMemcpyAsync(s_dev, s.data(), sizeof(int64_t) * m, cudaMemcpyHostToDevice,
+                                 cx.stream()));
+    FPM_TRY(pmbasis_rec_dev(cx, (uint32_t)p, F, m, n, fs, lf, order, s_dev, T, P, ps, sft_dev));
+    int deg = -1;
+    FPM_TRY(matrix_degree(cx, P, 0, (long long)m * m, (int)ps, &deg));  // synchronizes
+    *lp = deg + 1;
+    if (rdeg_out)
+      FPM_CUDA_TRY(cudaMemcpy(rdeg_out, sft_dev, sizeof(int64_t) * m, cudaMemcpyDeviceToHost));
+    return kOk;
+  }
   FPM_TRY(pmbasis_rec(cx, p, is64, F, m, n, fs, lf, order, s, T, P, ps, lp));
   if (rdeg_out) {
     std::vector<int64_t> rd;
