@@ -34,6 +34,24 @@ __global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* 
   }
 }
 
+// out[z][e][t] = in[e][t] mod prime z (u32), t < len: lets wide or unreduced
+// inputs use the persistent u32 NTT (one cheap streaming pass)
+__global__ void split_reduce_kernel(const void* in, int in64, int reduce, long long stride,
+                                    long long entries, int len, const __grid_constant__ PrimeSet ps,
+                                    uint32_t* out) {
+  const PrimeConst& pc = ps.pr[blockIdx.y];
+  const long long total = entries * len;
+  uint32_t* o = out + (long long)blockIdx.y * total;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i / len;
+    const long long src = e * stride + (i - e * len);
+    const uint64_t raw = in64 ? ((const unsigned long long*)in)[src]
+                              : (uint64_t)((const uint32_t*)in)[src];
+    o[i] = reduce ? d_red64(raw, pc.p, pc.mu) : (uint32_t)raw;
+  }
+}
+
 __global__ void zero_tail_kernel(void* out, int is64, long long stride, long long entries,
                                  int from, int to) {
   const int w = to - from;
@@ -183,6 +201,21 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   fb.reduce = reduce_needed || (!direct && B.is64);
   if (direct && B.is64) fb.reduce = 0;
   fb.n_entries = (int)eb; fb.out = EB; fb.out_prime_stride = N * eb;
+  // u64 / unreduced operands: one split-reduce pass, then the persistent
+  // u32 transform (all primes at once) instead of the generic kernel
+  auto to_u32 = [&](NttFwdArgs& f, long long entries) -> int {
+    if (!(f.in64 || f.reduce) || f.fold || f.len <= 0 || logn > 13) return kOk;
+    uint32_t* buf;
+    FPM_TRY(ws.get((size_t)r * entries * f.len, &buf));
+    dim3 g((unsigned)grid_for(entries * f.len), (unsigned)r);
+    split_reduce_kernel<<<g, 256, 0, st>>>(f.in, f.in64, f.reduce, f.in_stride, entries, f.len,
+                                           ps, buf);
+    FPM_LAUNCH_CHECK();
+    f.in = buf; f.in64 = 0; f.reduce = 0; f.in_stride = f.len;
+    f.in_prime_stride = entries * f.len;
+    return kOk;
+  };
+  FPM_TRY(to_u32(fb, eb));
   bool a_cached = false;
   if (cache) {
     const int pm_now = use_tc ? 1 : 0, pl_now = pq ? 2 : 5;
@@ -214,6 +247,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // both operands in one launch when their transforms are alike (persistent
   // grid: one tail wave instead of two)
   static const bool no_pair = std::getenv("FPM_NTT_NO_PAIR") != nullptr;
+  if (!a_cached) FPM_TRY(to_u32(fa, ea));
   if (a_cached) {
     StageTimer t_(cx, "ntt_fwd_B");
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
