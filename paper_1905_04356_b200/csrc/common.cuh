@@ -131,6 +131,7 @@ struct PrimeConst {
   uint32_t ninv_sh;  // Shoup companion of ninv
   const uint2* tw;   // forward twiddle rows: tw[r*32 + k] = w^(r*k), N entries
   const uint2* itw;  // inverse rows: w^-(r*k), N entries
+  const uint2* itw_s;  // inverse rows times N^-1 (ntt_tma.cu last pass)
   uint2 w32[16];     // (w32^e, Shoup) e < 16, w32 = w^(N/32): inner radix-32 DFTs
   uint2 iw32[16];    // inverse roots
   uint2 sc[4];       // (2^(8q) mod p, Shoup), q = 0..3: limb scaling (tc_pointwise.cu)

@@ -73,6 +73,12 @@ bool ntt_persist_inv_ok(int logn, const NttInvArgs& a);
 int launch_ntt_fwd_persist(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
 int launch_ntt_inv_persist(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// grouped TMA-fed kernels (ntt_tma.cu) for N = 2^11..2^13, blocked / quad layouts
+bool ntt_tma_fwd_ok(int logn, const NttFwdArgs& a);
+bool ntt_tma_inv_ok(int logn, const NttInvArgs& a);
+int launch_ntt_fwd_tma(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
+int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 // word offset of the 16-byte piece holding points x0 .. x0+3 (x0 % 4 == 0)
 // of entry e in the blocked eval layout E[N / 2^pl][n_entries][2^pl]
 __host__ __device__ __forceinline__ long long eval_piece(int x0, long long e, long long n_entries,

@@ -94,6 +94,62 @@ __device__ __forceinline__ void dit_small(uint32_t (&v)[32], const uint2* w, uin
   }
 }
 
+template <int R>
+__host__ __device__ constexpr int brev_r(int i) {
+  int r = 0;
+  for (int b = 0; b < R; ++b)
+    if (i & (1 << b)) r |= 1 << (R - 1 - b);
+  return r;
+}
+// register index of DIT-space index i: identity, or the low-R-bit reversal
+template <int R, bool ALIAS>
+__host__ __device__ constexpr int dit_ix(int i) {
+  return ALIAS ? ((i & ~((1 << R) - 1)) | brev_r<R>(i & ((1 << R) - 1))) : i;
+}
+
+// radix-2^R DIT over the low R bits with lazy reductions (ntt_tma.cu).
+//  * ALIAS = false: bit-reversed -> natural (inverse passes).
+//  * ALIAS = true: the same butterflies on registers renamed by the R-bit
+//    reversal compute the DFT of naturally ordered values and leave X[k] in
+//    register brev(k) -- exactly the DIF placement -- so forward passes use it
+//    too (the network and the results are the DIF ones).
+//  * A value that the next stage only multiplies (a b-operand with a nonzero
+//    twiddle) skips its reduction: the Shoup multiply accepts any input
+//    < 2^32 and the sums / differences stay < 2p < 2^32.  LAZY_OUT extends
+//    this to the last stage when a row-twiddle multiply follows every value.
+//  * HALF_ZERO (forward, R = 5): the upper 16 natural inputs are zero, so the
+//    first stage is a copy (u, 0) -> (u, u).
+// Inputs must be < p.
+template <int R, bool ALIAS, bool LAZY_OUT, bool HALF_ZERO = false>
+__device__ __forceinline__ void dit_lazy(uint32_t (&v)[32], const uint2* w, uint32_t p) {
+#pragma unroll
+  for (int hb = 0; hb < R; ++hb) {
+    const int h = 1 << hb;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (i & h) continue;
+      const int a = dit_ix<R, ALIAS>(i), b = dit_ix<R, ALIAS>(i + h);
+      if (HALF_ZERO && hb == 0) {
+        v[b] = v[a];
+        continue;
+      }
+      const int e = (i & (h - 1)) * (16 / h);
+      bool lazy_a = LAZY_OUT, lazy_b = LAZY_OUT;
+      if (hb < R - 1) {
+        const int h2 = 2 * h;
+        lazy_a = (i & h2) && (i & (h2 - 1));
+        lazy_b = ((i + h) & h2) && ((i + h) & (h2 - 1));
+      }
+      uint32_t t = v[b];
+      if (e) t = d_red(d_shoup(t, w[e].x, w[e].y, p), p);
+      const uint32_t u = v[a];
+      const uint32_t s = u + t, d = u - t + p;
+      v[a] = lazy_a ? s : d_red(s, p);
+      v[b] = lazy_b ? d : d_red(d, p);
+    }
+  }
+}
+
 // split load / apply so a row's 16-byte loads are issued a whole radix-32
 // DFT (or smem exchange) ahead of their use
 struct Row {

@@ -88,6 +88,7 @@ Context::~Context() {
   for (auto& kv : plans_) {
     cudaFree(kv.second.tw);
     cudaFree(kv.second.itw);
+    cudaFree(kv.second.itw_s);
   }
   if (pinned_) cudaFreeHost(pinned_);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
@@ -195,6 +196,18 @@ int Context::plan(uint32_t p, int logn, const Plan** out) {
   FPM_CUDA_TRY(cudaMalloc(&pl.itw, N * sizeof(uint2)));
   FPM_CUDA_TRY(cudaMemcpy(pl.tw, tw.data(), N * sizeof(uint2), cudaMemcpyHostToDevice));
   FPM_CUDA_TRY(cudaMemcpy(pl.itw, itw.data(), N * sizeof(uint2), cudaMemcpyHostToDevice));
+  {
+    // inverse rows pre-multiplied by N^-1: the last inverse pass applies its
+    // row twiddles to all 32 values (k = 0 included), which also scales
+    const uint64_t ni = h_invmod(N % p, p);
+    std::vector<uint2> its(N);
+    for (size_t i = 0; i < N; ++i) {
+      const uint32_t w = (uint32_t)h_mulmod(itw[i].x, ni, p);
+      its[i] = make_uint2(w, h_shoup(w, p));
+    }
+    FPM_CUDA_TRY(cudaMalloc(&pl.itw_s, N * sizeof(uint2)));
+    FPM_CUDA_TRY(cudaMemcpy(pl.itw_s, its.data(), N * sizeof(uint2), cudaMemcpyHostToDevice));
+  }
   // radix-32 inner roots w32 = omega^(N/32) (logn >= 5 in every kernel)
   const uint64_t w32 = h_powmod(omega, N >= 32 ? N / 32 : 1, p), iw32 = h_invmod(w32, p);
   uint64_t a = 1, b = 1;
@@ -271,6 +284,7 @@ int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   }
   out->tw = pl->tw;
   out->itw = pl->itw;
+  out->itw_s = pl->itw_s;
   for (int e = 0; e < 16; ++e) {
     out->w32[e] = pl->w32[e];
     out->iw32[e] = pl->iw32[e];

@@ -14,6 +14,7 @@ struct Plan {
   int logn = 0;
   uint2* tw = nullptr;   // device, N entries (twiddle rows, see ntt.cu)
   uint2* itw = nullptr;  // device, N entries
+  uint2* itw_s = nullptr;  // device, N entries: itw * N^-1 (last inverse pass, ntt_tma.cu)
   uint32_t ninv = 0, ninv_sh = 0;
   uint2 w32[16], iw32[16];
 };
