@@ -36,6 +36,7 @@ struct F31 {
   uint32_t p, pinv;  // pinv = -p^-1 mod 2^32
   uint64_t mu;       // floor(2^64 / p)
   uint32_t c32;      // 2^32 mod p
+  uint32_t r2;       // 2^64 mod p (into the Montgomery domain)
 };
 
 // (a*w + (p-b)*y) * 2^-32 mod p, all inputs < p, result < p
@@ -61,21 +62,111 @@ __device__ __forceinline__ uint32_t redc_mul(uint32_t a, uint32_t b, const F31& 
 
 // a^(p-2) by square-and-multiply in the Montgomery domain (cheaper products
 // than Barrett; x -> x 2^32 on entry via r2 = 2^64 mod p, 2^-32 on exit)
+// (r2 precomputed on the host: a 128-bit modulo here costs thousands of cycles)
 __device__ uint32_t invmod(uint32_t a, const F31& f) {
-  const uint32_t r2 = (uint32_t)((((unsigned __int128)1) << 64) % f.p);
-  uint32_t b = redc_mul(a, r2, f);           // a R
-  uint32_t r = redc_mul(1u, r2, f);          // R
-  uint32_t e = f.p - 2;
-  while (e) {
-    if (e & 1) r = redc_mul(r, b, f);
+  uint32_t b = redc_mul(a, f.r2, f);         // a R
+  uint32_t r = redc_mul(1u, f.r2, f);        // R
+  const uint32_t e = f.p - 2;                // < 2^31: 31 right-to-left steps
+#pragma unroll
+  for (int i = 0; i < 31; ++i) {
+    const uint32_t rb = redc_mul(r, b, f);   // independent of the squaring chain
+    r = (e >> i) & 1u ? rb : r;
     b = redc_mul(b, b, f);
-    e >>= 1;
   }
   return redc_mul(r, 1u, f);                 // out of the Montgomery domain
 }
 
 __device__ __forceinline__ uint64_t fold(uint64_t acc, uint32_t c32) {
   return (uint64_t)(uint32_t)(acc >> 32) * c32 + (uint32_t)acc;
+}
+
+// (d*v - al*x - be*y) * 2^-32 mod p, all inputs < p, result < p
+__device__ __forceinline__ uint32_t redc3(uint32_t d, uint32_t v, uint32_t al, uint32_t x,
+                                          uint32_t be, uint32_t y, const F31& f) {
+  uint64_t acc = (uint64_t)d * v + (uint64_t)(f.p - al) * x + (uint64_t)(f.p - be) * y;  // < 3p^2
+  acc = fold(acc, f.c32);                                 // < 2^63, same residue
+  const uint32_t m = (uint32_t)acc * f.pinv;
+  const uint32_t t = (uint32_t)((acc + (uint64_t)m * f.p) >> 32);  // < 2p
+  return min(t, t - f.p);
+}
+
+// Generic canonical step for n = NC pivot columns, m <= 64 rows, 512 threads:
+// Gauss-Jordan on [R_P^T | R_K^T] (NC x m; R_P = the NC lowest-ranked rows
+// of the residual, R_K = the others in index order), TWO columns per barrier.
+// For the 2 x 2 pivot block [[a, b], [d, e]] (rows c, c+1) and any other row
+// with entries (x, y) in those columns,
+//    row <- D row - (x e - y d) row_c - (y a - x b) row_{c+1},  D = a e - b d,
+//    row_c <- e row_c - b row_{c+1},  row_{c+1} <- a row_{c+1} - d row_c
+// clear both columns (every row picks up a nonzero factor, harmless).  With
+// a != 0 and D != 0 at every block all leading principal minors of R_P are
+// nonzero, so the reference's column elimination (appint.py:41-58) takes
+// exactly the rows in rank order as pivots and the kernel coefficients are the
+// unique C = R_K R_P^-1; the left block ends diagonal (d_q) and the right
+// block is D C^T, so Ct[q][kr] = -right[q][kr] / d_q with no product phase.
+// Thread (gi, gs) holds row gi, columns gs + 16u.  Returns false (uniformly)
+// on a zero leading minor; W and the shared step state are then untouched.
+template <int NC>
+__device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int* klist,
+                            uint32_t* pbuf, const F31& f, uint32_t* Ct, uint32_t* recC,
+                            unsigned long long* trace) {
+  const int tid = threadIdx.x, gi = tid >> 4, gs = tid & 15;
+  const int nk = m - NC;
+  uint32_t v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int col = gs + 16 * u;
+    v[u] = col < NC ? W[ord[col] * NC + gi] : (col < m ? W[klist[col - NC] * NC + gi] : 0u);
+  }
+#pragma unroll
+  for (int c = 0; c < NC; c += 2) {
+    uint32_t* pb = pbuf + ((c >> 1) & 1) * 128;
+    if (gi == c) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pb[gs + 16 * u] = v[u];
+    } else if (gi == c + 1) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pb[64 + gs + 16 * u] = v[u];
+    }
+    __syncthreads();
+    const uint32_t a = pb[c], b = pb[c + 1], d = pb[64 + c], e = pb[64 + c + 1];
+    const uint32_t dl = redc_axby(a, e, b, d, f);
+    if (a == 0 || dl == 0) return false;  // every thread read the same block
+    if (trace && c == 0 && tid == 0) trace[7] = clock64();
+    const uint32_t x = __shfl_sync(0xffffffffu, v[c >> 4], c & 15, 16);
+    const uint32_t y = __shfl_sync(0xffffffffu, v[(c + 1) >> 4], (c + 1) & 15, 16);
+    uint32_t rc[4], rd[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      rc[u] = pb[gs + 16 * u];
+      rd[u] = pb[64 + gs + 16 * u];
+    }
+    if (gi == c) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = redc_axby(e, rc[u], b, rd[u], f);
+    } else if (gi == c + 1) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = redc_axby(a, rd[u], d, rc[u], f);
+    } else {
+      const uint32_t al = redc_axby(x, e, y, d, f), be = redc_axby(y, a, x, b, f);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = redc3(dl, v[u], al, rc[u], be, rd[u], f);
+    }
+  }
+  if (trace && tid == 0) trace[6] = clock64();
+  // d_q = M[q][q] from the row's own threads; every thread of row q inverts it
+  const uint32_t dq = __shfl_sync(0xffffffffu, (gi >> 4) ? v[1] : v[0], gi & 15, 16);
+  const uint32_t iq = invmod(dq, f);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int col = gs + 16 * u;
+    if (col >= NC && col < m) {
+      const uint32_t c = mulmod(v[u], iq, f);
+      const uint32_t val = c ? f.p - c : 0u;
+      Ct[gi * nk + col - NC] = val;
+      recC[gi * nk + col - NC] = val;
+    }
+  }
+  return true;
 }
 
 struct StepArgs {
@@ -116,7 +207,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   int* klist = plist + m;                         // m
   __shared__ int s_key[2];
   __shared__ int s_nk;
-  __shared__ uint32_t sbuf[2 * 96];  // block solve: pivot row + column, double buffered
+  __shared__ uint32_t sbuf[2 * 128];  // block solves: pivot rows (+ column), double buffered
 
   const int hw = tid >> 4, l16 = tid & 15;  // half-warp per row
   constexpr int kRowsPerPass = kStepThreads / 16;
@@ -131,8 +222,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   for (int k = 0; k < T; ++k) {
     const uint32_t* Gk = G + (size_t)k * mn;
     for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
-    const bool try_fast = m > n && n <= 32 && 2 * n * n + n * (m - n + 1) <= m * m;
-    if (!try_fast)
+    const bool pairs_shape = n == 32 && m > n && m <= 64;  // solve_pairs
+    const bool try_fast = !pairs_shape && m > n && n <= 32 && 2 * n * n + n * (m - n + 1) <= m * m;
+    if (!try_fast && !pairs_shape)
       for (int idx = tid; idx < m * m; idx += kStepThreads)
         X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
     // rank of row i by (s_i, i): 8 threads per row, shuffle-reduced
@@ -165,7 +257,35 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     // barrier per column, pivot row / column broadcast through double-
     // buffered shared memory) plus one dense product give C; a zero leading
     // minor (degenerate residual) falls back to the general elimination.
-    bool fast_done = false;
+    bool fast_done = false, pairs_done = false;
+    if (n == 32 && m > n && m <= 64) {
+      // pivots = the n lowest-ranked rows; kernel rows in index order
+      for (int i = tid; i < m; i += kStepThreads) piv[i] = rank[i] < n ? 1 : 0;
+      for (int q = tid; q < n; q += kStepThreads) plist[q] = ord[q];
+      if (tid < 32) {  // warp 0: klist by ballot / popc prefix over the m rows
+        int base = 0;
+        for (int i0 = 0; i0 < m; i0 += 32) {
+          const int i = i0 + tid;
+          const bool kr = i < m && rank[i] >= n;
+          const unsigned bal = __ballot_sync(0xffffffffu, kr);
+          if (kr) klist[base + __popc(bal & ((1u << tid) - 1u))] = i;
+          base += __popc(bal);
+        }
+        if (tid == 0) s_nk = base;
+      }
+      __syncthreads();
+      if (solve_pairs<32>(W, m, ord, klist, sbuf, f, W, a.rec_Ct + (size_t)k * m * m,
+                          a.trace ? a.trace + k * 8 : nullptr)) {
+        fast_done = pairs_done = true;
+      } else {
+        // degenerate residual: the general elimination starts from X = I
+        for (int i = tid; i < m; i += kStepThreads) piv[i] = 0;
+        for (int idx = tid; idx < m * m; idx += kStepThreads)
+          X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
+      }
+      __syncthreads();
+      STEP_TRACE(5);
+    }
     const int n2 = 2 * n;
     uint32_t* A = X;                          // [n][2n] after the solve
     uint32_t* Cs = X + (size_t)n * n2;        // Ct [n][m-n+1] (padded rows)
@@ -334,7 +454,9 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     if (np == 0) continue;  // R = 0: nothing changes (appint.py:171)
     uint32_t* Ct = W;  // compact [np][nk]
     uint32_t* recC = a.rec_Ct + (size_t)k * m * m;
-    if (fast_done) {
+    if (pairs_done) {
+      // solve_pairs wrote Ct (here, in W) and the record
+    } else if (fast_done) {
       for (int idx = tid; idx < np * nk; idx += kStepThreads) {
         const int q = idx / nk, kr = idx - (idx / nk) * nk;
         const uint32_t v = Cs[q * (nk + 1) + kr];
@@ -536,6 +658,7 @@ F31 make_f31(uint32_t p) {
   f.pinv = 0u - inv;
   f.mu = (uint64_t)((((u128)1) << 64) / p);
   f.c32 = (uint32_t)(((uint64_t)1 << 32) % p);
+  f.r2 = (uint32_t)((((u128)1) << 64) % p);
   return f;
 }
 

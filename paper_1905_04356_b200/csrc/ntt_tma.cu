@@ -81,6 +81,7 @@ struct TmaFwdArgs {
   int len;       // coefficients per entry (multiple of 4)
   int in_words;  // input buffer words: N/2 (upper half zero) or N
   int pl;        // eval block log: 5 (E[N/32][e][32]) or 2 (E[N/4][e][4])
+  int diag;      // FPM_NTT_DIAG bit 0: skip the output stores (timing experiments only)
 };
 
 struct TmaInvArgs {
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
           make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     tc::fence_proxy_async();
     gsync(bar, T::TPT);
-    if (leader) {
+    if (leader && !(a.diag & 1)) {
       const bool second = item >= a.n1;
       const CUtensorMap* om = second ? &om2 : &om1;
       const int e = (int)(second ? item - a.n1 : item);
@@ -313,8 +314,10 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
   uint8_t* tab = sm;
   uint8_t* tile8 = sm + T::TAB_BYTES + g * T::TILE_BYTES;
   uint32_t* tile = reinterpret_cast<uint32_t*>(tile8);
-  uint64_t* mb = reinterpret_cast<uint64_t*>(sm + T::TAB_BYTES + G * T::TILE_BYTES) + g;
-  const uint32_t mbar = smem_u32(mb), tile_s = smem_u32(tile8);
+  // evaluations land in a separate buffer, a whole transform ahead
+  uint8_t* inb8 = sm + T::TAB_BYTES + G * T::TILE_BYTES + g * T::N * 4;
+  uint64_t* mb = reinterpret_cast<uint64_t*>(sm + T::TAB_BYTES + G * (T::TILE_BYTES + T::N * 4)) + g;
+  const uint32_t mbar = smem_u32(mb), inb_s = smem_u32(inb8);
 
   stage_tables<LOGN, G>(tab, pc.itw_s, pc.itw);
   if (leader) {
@@ -330,10 +333,10 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
   auto load = [&](long long it) {
     expect_tx(mbar, (uint32_t)T::N * 4u);
     if constexpr (PL == 5) {
-      tc::tma_load_4d(tile_s, &im, mb, 0, (int)it, 0, z);
+      tc::tma_load_4d(inb_s, &im, mb, 0, (int)it, 0, z);
     } else {
 #pragma unroll
-      for (int c = 0; c < 8; ++c) tma_load_5d(tile_s + c * (T::N / 2), &im, mbar, 0, (int)it, c, 0, z);
+      for (int c = 0; c < 8; ++c) tma_load_5d(inb_s + c * (T::N / 2), &im, mbar, 0, (int)it, c, 0, z);
     }
   };
   if (leader && item < a.n) load(item);
@@ -344,14 +347,17 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
     tc::mbar_wait_a(mbar, phase);
     phase ^= 1u;
     uint32_t v[32];
-    // dense row lt (points 32 lt ..) of the SWIZZLE_128B tile
+    // row lt (points 32 lt .. 32 lt + 31) of the landed evaluations
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
-      const uint4 t = *reinterpret_cast<const uint4*>(tile8 + chunk_off<LOGN, PL>(lt, c));
+      const uint4 t = *reinterpret_cast<const uint4*>(inb8 + chunk_off<LOGN, PL>(lt, c));
       v[4 * c] = t.x; v[4 * c + 1] = t.y; v[4 * c + 2] = t.z; v[4 * c + 3] = t.w;
     }
     dit_lazy<T::LAST_R, false, true>(v, pc.iw32, p);
-    gsync(bar, T::TPT);  // dense reads done before the padded exchange writes
+    // input buffer read by every thread (the next transform may land), and the
+    // previous transform's last tile reads are done (tile free)
+    gsync(bar, T::TPT);
+    if (leader && item + step < a.n) load(item + step);
     to_smem<LOGN, MAP_LAST>(tile, v, lt);
     gsync(bar, T::TPT);
     from_smem<LOGN, MAP_MID>(tile, v, lt);
@@ -360,9 +366,6 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
     to_smem<LOGN, MAP_MID>(tile, v, lt);  // own positions
     gsync(bar, T::TPT);
     from_smem<LOGN, MAP_TOP>(tile, v, lt);
-    tc::fence_proxy_async();  // generic tile writes ordered before the TMA overwrite
-    gsync(bar, T::TPT);  // tile free: the next transform's evaluations land during this pass
-    if (leader && item + step < a.n) load(item + step);
     row_apply_t<true>(v, top_row, p);  // twiddles times N^-1
     dit_lazy<5, false, false>(v, pc.iw32, p);
     uint32_t* oe = a.out + z * a.out_ps + item * a.out_stride;
@@ -489,7 +492,7 @@ size_t fwd_smem(int len) {
 template <int LOGN, int G>
 size_t inv_smem() {
   using T = TG<LOGN, G>;
-  return 1024 + T::TAB_BYTES + (size_t)G * T::TILE_BYTES + 8 * G;
+  return 1024 + T::TAB_BYTES + (size_t)G * (T::TILE_BYTES + T::N * 4) + 8 * G;
 }
 
 long long grid_x(long long items, int G, int primes) {
@@ -512,6 +515,8 @@ int fwd_launch(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t st) {
   a.len = f.len;
   a.in_words = f.len <= T::N / 2 ? T::N / 2 : T::N;
   a.pl = f.pblk_log ? f.pblk_log : 5;
+  static const int diag = std::getenv("FPM_NTT_DIAG") ? std::atoi(std::getenv("FPM_NTT_DIAG")) : 0;
+  a.diag = diag;
   CUtensorMap m1, m2;
   FPM_TRY(make_eval_map(&m1, f.out, f.n_entries, T::N, a.pl, f.out_prime_stride, ps.count));
   if (two)
@@ -601,7 +606,7 @@ int launch_ntt_fwd_tma(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaSt
 }
 
 int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  const bool big = tma_threads() == 768;
+  const bool big = tma_threads() == 768 && logn == 11;  // 3 groups of 2^12/2^13 do not fit
   return (a.pblk_log == 2) ? inv_pl<2>(logn, big, a, ps, st) : inv_pl<5>(logn, big, a, ps, st);
 }
 

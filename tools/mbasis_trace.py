@@ -23,11 +23,14 @@ def main():
     buf = (ctypes.c_ulonglong * 512)()
     assert _lib.lib().fpm_debug_mbasis_trace(buf) == 0
     names = ["solve", "inv", "C", "Ct", "residual", "shift", "next_start"]
+    print("pair path: solve = [start, first block] [pair loop] [inverses]")
     print("step " + " ".join(f"{n:>10s}" for n in names))
     for k in range(16):
         r = [buf[k * 8 + e] for e in range(8)]
         nxt = buf[(k + 1) * 8] if k < 15 else r[4]
-        if r[5] and r[6]:
+        if r[7] and r[6] and r[5]:
+            d = [r[7] - r[0], r[6] - r[7], r[5] - r[6]]
+        elif r[5] and r[6]:
             d = [r[5] - r[0], r[6] - r[5], r[1] - r[6]]
         else:
             d = [r[1] - r[0], 0, 0]
