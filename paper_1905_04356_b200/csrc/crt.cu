@@ -115,16 +115,37 @@ __global__ void middle_entrywise_kernel(MiddleEntryArgs a) {
   }
 }
 
+// max over entries of the trimmed length: one warp per entry scans 128-value
+// chunks from the end (coalesced, 4 loads in flight) and stops at the first
+// chunk holding a nonzero coefficient
 template <typename T>
 __global__ void max_len_kernel(const T* M, long long entries, int L, int* out) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
   int best = 0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < entries;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int l = trimmed_len(M + e * L, L);
-    best = l > best ? l : best;
+  for (long long e = w0; e < entries; e += nw) {
+    const T* row = M + e * L;
+    for (int hi = L; hi > best; hi -= 128) {
+      T v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int t = hi - 128 + 32 * q + lane;
+        v[q] = t >= 0 && t < hi ? row[t] : (T)0;
+      }
+      int found = 0;
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const unsigned bal = __ballot_sync(0xffffffffu, v[q] != 0);
+        if (!found && bal) found = hi - 128 + 32 * q + 32 - __clz(bal);
+      }
+      if (found) {
+        best = max(best, found);
+        break;
+      }
+    }
   }
-  for (int o = 16; o; o >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, o));
-  if ((threadIdx.x & 31) == 0 && best > 0) atomicMax(out, best);
+  if (lane == 0 && best > 0) atomicMax(out, best);
 }
 
 template <typename T>
@@ -240,7 +261,7 @@ int launch_middle_entrywise(const MiddleEntryArgs& a, cudaStream_t st) {
 int launch_max_len(const void* M, int in64, long long entries, int L, int* out, cudaStream_t st) {
   FPM_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(int), st));
   if (entries <= 0 || L <= 0) return kOk;
-  long long blocks = (entries + 255) / 256;
+  long long blocks = (entries * 32 + 255) / 256;  // one warp per entry
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (in64)
     max_len_kernel<uint64_t><<<(unsigned)blocks, 256, 0, st>>>((const uint64_t*)M, entries, L, out);

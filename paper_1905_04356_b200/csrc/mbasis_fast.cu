@@ -578,68 +578,111 @@ struct BuildArgs {
   F31 f;
 };
 
-// one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j
+// one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j.  Every step's
+// record (pivot list, compact Ct) is staged into shared memory up front with
+// cp.async (all loads in flight) and the per-step row maps are built in
+// parallel; a step then gathers the pivot rows' coefficients (and shifts
+// them by x) and computes the kernel rows P1[t][klist[kr]] = P0[t][klist[kr]]
+// + sum_q Ct[q][kr] P0[t][plist[q]] with independent shared loads.
 __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
   extern __shared__ __align__(16) uint32_t bsm[];
   const int m = a.m, T = a.T, j = blockIdx.x;
   const int tid = threadIdx.x, NT = blockDim.x;
   const int L1 = T + 1;
-  uint32_t* P0 = bsm;                   // [L1][m]
-  uint32_t* P1 = bsm + (size_t)L1 * m;  // [L1][m]
-  int* isp = (int*)(bsm + 2 * (size_t)L1 * m + (size_t)m * m);  // m: pivot index q or -1 (after Ct)
-  int* kidx = isp + m;                  // m: kernel index kr or -1
-  int* plist = kidx + m;                // m
+  const int cmax = (m / 2) * ((m + 1) / 2);  // np * nk <= m^2 / 4
+  uint32_t* P0 = bsm;                                     // [L1][m]
+  uint32_t* P1 = P0 + (size_t)L1 * m;                     // [L1][m]
+  uint32_t* Pp = P1 + (size_t)L1 * m;                     // [L1][m] gathered pivot rows
+  uint32_t* Cs = Pp + (size_t)L1 * m;                     // [T][cmax] compact Ct
+  int* nps = (int*)(Cs + (size_t)T * cmax);               // [T]
+  short* plist = (short*)(nps + T);                       // [T][m]
+  short* klist = plist + (size_t)T * m;                   // [T][m]
+  short* isp = klist + (size_t)T * m;                     // [T][m]: pivot flag
+  {
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(Cs);
+    for (int k = 0; k < T; ++k) {
+      const int cnt = a.rec_np[k] * (m - a.rec_np[k]);
+      for (int c = tid; c < cnt; c += NT)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                         base + 4u * (uint32_t)(k * cmax + c)),
+                     "l"(a.rec_Ct + (size_t)k * m * m + c));
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  for (int k = tid; k < T; k += NT) nps[k] = a.rec_np[k];
+  for (int idx = tid; idx < T * m; idx += NT) {
+    plist[idx] = (short)a.rec_plist[idx];
+    isp[idx] = 0;
+  }
   for (int idx = tid; idx < L1 * m; idx += NT) P0[idx] = (idx == j) ? 1u : 0u;
+  __syncthreads();
+  for (int idx = tid; idx < T * m; idx += NT) {
+    const int k = idx / m, q = idx - (idx / m) * m;
+    if (q < nps[k]) isp[k * m + plist[idx]] = 1;
+  }
+  __syncthreads();
+  {  // kernel rows in index order: ballot prefix, one warp per step
+    const int w = tid >> 5, lane = tid & 31;
+    for (int k = w; k < T; k += NT / 32) {
+      int base = 0;
+      for (int i0 = 0; i0 < m; i0 += 32) {
+        const int i = i0 + lane;
+        const bool kr = i < m && !isp[k * m + i];
+        const unsigned bal = __ballot_sync(0xffffffffu, kr);
+        if (kr) klist[k * m + base + __popc(bal & ((1u << lane) - 1u))] = (short)i;
+        base += __popc(bal);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  const bool k4 = a.fold_k >= 4;
   int L = 1;
   for (int k = 0; k < T; ++k) {
-    const int np = a.rec_np[k];
+    const int np = nps[k];
     if (np == 0) continue;  // R = 0: the reference leaves P unchanged
-    __syncthreads();
-    for (int i = tid; i < m; i += NT) isp[i] = -1;
-    __syncthreads();
-    for (int q = tid; q < np; q += NT) {
-      const int l = a.rec_plist[(size_t)k * m + q];
-      plist[q] = l;
-      isp[l] = q;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int nk = 0;
-      for (int i = 0; i < m; ++i) kidx[i] = isp[i] < 0 ? nk++ : -1;
-    }
-    __syncthreads();
     const int nk = m - np;
-    uint32_t* Ct = bsm + 2 * (size_t)L1 * m;  // staged [np][nk] (fixed, after both P buffers)
-    {
-      const uint32_t* g = a.rec_Ct + (size_t)k * m * m;
-      for (int idx = tid; idx < np * nk; idx += NT) Ct[idx] = g[idx];
+    const uint32_t* Ct = Cs + (size_t)k * cmax;
+    const short* pl = plist + k * m;
+    const short* kl = klist + k * m;
+    // pivot rows: gather (t < L) and shift by x into P1 (t = 0 .. L)
+    for (int idx = tid; idx < (L + 1) * np; idx += NT) {
+      const int t = idx / np, q = idx - (idx / np) * np;
+      const int i = pl[q];
+      if (t < L) Pp[t * m + q] = P0[(size_t)t * m + i];
+      P1[(size_t)t * m + i] = t >= 1 ? P0[(size_t)(t - 1) * m + i] : 0u;
     }
     __syncthreads();
-    for (int idx = tid; idx < (L + 1) * m; idx += NT) {
-      const int t = idx / m, i = idx - (idx / m) * m;
+    for (int idx = tid; idx < (L + 1) * nk; idx += NT) {
+      const int t = idx / nk, kr = idx - (idx / nk) * nk;
+      const int i = kl[kr];
       uint32_t v = 0;
-      if (isp[i] >= 0) {
-        if (t >= 1) v = P0[(size_t)(t - 1) * m + i];
-      } else if (t < L) {
-        const int kr = kidx[i];
-        uint64_t acc = P0[(size_t)t * m + i];
-        int cnt = 0;
-        for (int q = 0; q < np; ++q) {
-          acc += (uint64_t)Ct[(size_t)q * nk + kr] * P0[(size_t)t * m + plist[q]];
-          if (++cnt == a.fold_k) {
-            cnt = 0;
-            acc = fold(acc, a.f.c32);
+      if (t < L) {
+        const uint32_t* pp = Pp + t * m;
+        uint64_t acc0 = P0[(size_t)t * m + i], acc1 = 0;
+        int q = 0;
+        if (k4) {
+          for (; q + 4 <= np; q += 4) {
+            acc0 += (uint64_t)Ct[(size_t)q * nk + kr] * pp[q];
+            acc1 += (uint64_t)Ct[(size_t)(q + 1) * nk + kr] * pp[q + 1];
+            acc0 += (uint64_t)Ct[(size_t)(q + 2) * nk + kr] * pp[q + 2];
+            acc1 += (uint64_t)Ct[(size_t)(q + 3) * nk + kr] * pp[q + 3];
+            acc0 = fold(acc0, a.f.c32);
+            acc1 = fold(acc1, a.f.c32);
           }
         }
-        v = d_red64(acc, a.f.p, a.f.mu);
+        for (; q < np; ++q) {
+          acc0 += (uint64_t)Ct[(size_t)q * nk + kr] * pp[q];
+          acc0 = fold(acc0, a.f.c32);
+        }
+        v = d_red(d_red64(acc0, a.f.p, a.f.mu) + d_red64(acc1, a.f.p, a.f.mu), a.f.p);
       }
-      P1[idx] = v;
+      P1[(size_t)t * m + i] = v;
     }
     __syncthreads();
     uint32_t* tmp = P0; P0 = P1; P1 = tmp;
     ++L;
   }
-  __syncthreads();
   // column j of P, entry-major: P[(i*m + j)*ps + t]
   const int ps = (int)a.ps;
   for (int idx = tid; idx < m * ps; idx += NT) {
@@ -671,12 +714,19 @@ size_t steps_smem(int m, int n, int T) {
 
 int fold_period(uint32_t p);  // pointwise.cu
 
+// mbasis_build_kernel: two P buffers, the compact records, row maps
+size_t build_smem(int m, int order) {
+  const size_t cmax = (size_t)(m / 2) * ((m + 1) / 2);
+  return 3 * (size_t)(order + 1) * m * 4 + (size_t)order * cmax * 4 + (size_t)order * 4 +
+         (size_t)order * m * 6 + 16;
+}
+
 int mbasis_fast_max_order(int m, int n) {
   // largest leaf order whose residual list fits in shared memory
   const size_t cap = 200 * 1024;
   if (2 * (size_t)2 * m * 4 > cap) return 0;
   int T = 0;
-  while (T < 64 && steps_smem(m, n, T + 1) <= cap && (size_t)(T + 2) * m * 8 + 12 * m <= cap) ++T;
+  while (T < 64 && steps_smem(m, n, T + 1) <= cap && build_smem(m, T + 1) <= cap) ++T;
   return T;
 }
 
@@ -719,7 +769,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   BuildArgs ba{};
   ba.rec_np = rec_np; ba.rec_plist = rec_plist; ba.rec_Ct = rec_Ct; ba.m = m; ba.T = order;
   ba.P = (uint32_t*)P; ba.ps = ps; ba.fold_k = K; ba.f = f;
-  const size_t bsmem = 2 * (size_t)(order + 1) * m * 4 + 4 * (size_t)m * m + 12 * (size_t)m;
+  const size_t bsmem = build_smem(m, order);
   static size_t battr = 0;
   if (bsmem > 48 * 1024 && bsmem > battr) {
     FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_build_kernel,
