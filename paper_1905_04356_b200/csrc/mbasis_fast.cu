@@ -169,6 +169,62 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
   return true;
 }
 
+// Residual-list update on R x 4 tiles (aligned shapes, folds every 4
+// products): G[t][klist[kr]][j] += sum_q Ct[q][kr] G[t][plist[q]][j] for the
+// kernel rows kr of one R-row block and 4 columns j.  Smaller R spreads a
+// short list (few t) over all threads instead of leaving most of them idle.
+template <int R>
+__device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct, const int* klist,
+                                               const int* plist, int n, int nk, int np, int k,
+                                               int nt, size_t mn, const F31& f) {
+  const int rb_n = nk / R, cb_n = n >> 2;
+  const int blocks = rb_n * cb_n * nt;
+  for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
+    const int t = k + 1 + b / (rb_n * cb_n);
+    const int rem = b - (b / (rb_n * cb_n)) * (rb_n * cb_n);
+    const int rb = rem / cb_n, cb = rem - (rem / cb_n) * cb_n;
+    uint32_t* Gt = G + (size_t)t * mn;
+    int rows[R];
+    uint64_t acc[R][4];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      rows[r] = klist[rb * R + r];
+      const uint4 g = *reinterpret_cast<const uint4*>(Gt + (size_t)rows[r] * n + cb * 4);
+      acc[r][0] = g.x; acc[r][1] = g.y; acc[r][2] = g.z; acc[r][3] = g.w;
+    }
+#pragma unroll 4
+    for (int q = 0; q < np; ++q) {
+      const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + (size_t)plist[q] * n + cb * 4);
+      const uint32_t gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      uint32_t cv[R];
+      if constexpr (R == 4) {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(Ct + q * nk + rb * 4);
+        cv[0] = c4.x; cv[1] = c4.y; cv[2] = c4.z; cv[3] = c4.w;
+      } else if constexpr (R == 2) {
+        const uint2 c2 = *reinterpret_cast<const uint2*>(Ct + q * nk + rb * 2);
+        cv[0] = c2.x; cv[1] = c2.y;
+      } else {
+        cv[0] = Ct[q * nk + rb];
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) acc[r][cc] += (uint64_t)cv[r] * gv[cc];
+      if ((q & 3) == 3) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) acc[r][cc] = fold(acc[r][cc], f.c32);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      *reinterpret_cast<uint4*>(Gt + (size_t)rows[r] * n + cb * 4) =
+          make_uint4(d_red64(acc[r][0], f.p, f.mu), d_red64(acc[r][1], f.p, f.mu),
+                     d_red64(acc[r][2], f.p, f.mu), d_red64(acc[r][3], f.p, f.mu));
+  }
+}
+
 struct StepArgs {
   const uint32_t* F;
   long long fs;
@@ -480,7 +536,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     STEP_TRACE(2);
 
     // ---- residual list: kernel rows G[t][i] += sum_q Ct G[t][plist[q]], t > k -
-    {
+    if (((n | nk) & 3) == 0 && a.fold_k == 4) {
+      const int nt = T - k - 1;
+      if (nt <= 2)
+        residual_tiles<1>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+      else if (nt <= 4)
+        residual_tiles<2>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+      else
+        residual_tiles<4>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+    } else {
       const int rb_n = (nk + 3) >> 2, cb_n = (n + 3) >> 2, nt = T - k - 1;
       const int blocks = rb_n * cb_n * nt;
       const int K = a.fold_k;

@@ -455,7 +455,8 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
     // update (grows with the leaf order) against the tree's products
     // (cfg4: T = 16 179 ms, T = 8 168 ms, T = 4 184 ms)
     const int tf = mbasis_fast_max_order(m, n);
-    const int tcap = tf < 8 ? tf : 8;
+    static const int tmax = std::getenv("FPM_PMBASIS_TMAX") ? std::atoi(std::getenv("FPM_PMBASIS_TMAX")) : 8;
+    const int tcap = tf < tmax ? tf : tmax;
     if (tf >= 1 && T > tcap) T = tcap;
   }
   std::vector<int64_t> s(shift, shift + m);

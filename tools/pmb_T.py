@@ -20,7 +20,7 @@ def main():
     cfg = dict(bench.CONFIGS["cfg4"], sigma=sigma)
     F = bench.make_inputs(cfg, "cuda", 4)[0]
     ref = None
-    for T in (16, 8, 4, 2):
+    for T in [int(x) for x in os.environ.get('PMB_TS', '16,8,4,2').split(',')]:
         dense.pmbasis_dense(F, sigma, [0] * cfg["m"], cfg["p"], T=T)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
