@@ -121,6 +121,34 @@ __device__ __forceinline__ uint32_t d_red56(uint64_t x, uint32_t p, uint32_t m58
   return min(r, r - p);
 }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------
+// A kernel launched with launch_pdl() may start while the previous kernel in
+// the stream drains: its prologue (tables, barriers, TMEM, descriptors)
+// overlaps that kernel's tail and the launch latency.  Every such kernel
+// calls pdl_wait() before touching global data another kernel may write; it
+// is a no-op for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+bool pdl_enabled();  // runtime.cu: off under FPM_NO_PDL
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 // Per-prime constants handed to kernels by value (kernel-parameter space, so
 // the radix-32 root constants are constant-bank operands, not loads).
 struct PrimeConst {

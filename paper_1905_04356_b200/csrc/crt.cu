@@ -25,6 +25,7 @@ __device__ __forceinline__ uint64_t d_addmod64(uint64_t a, uint64_t b, uint64_t 
 namespace {
 
 __global__ void crt_kernel(CrtArgs a) {
+  pdl_wait();
   const long long total = (long long)a.n_entries * a.len;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -67,6 +68,7 @@ __device__ __forceinline__ int trimmed_len(const T* e, int L) {
 
 template <typename Tin, typename Tout>
 __global__ void middle_entrywise_kernel(MiddleEntryArgs a) {
+  pdl_wait();
   const Tin* A = (const Tin*)a.A;
   const Tin* B = (const Tin*)a.B;
   Tout* out = (Tout*)a.out;
@@ -120,6 +122,7 @@ __global__ void middle_entrywise_kernel(MiddleEntryArgs a) {
 // chunk holding a nonzero coefficient
 template <typename T>
 __global__ void max_len_kernel(const T* M, long long entries, int L, int* out) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long w0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
@@ -150,6 +153,7 @@ __global__ void max_len_kernel(const T* M, long long entries, int L, int* out) {
 
 template <typename T>
 __global__ void rdeg_kernel(const T* M, int rows, int cols, int L, const int64_t* s, int64_t* out) {
+  pdl_wait();
   // one warp per row
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -169,6 +173,7 @@ __global__ void rdeg_kernel(const T* M, int rows, int cols, int L, const int64_t
 
 __global__ void dft_direct_kernel(uint64_t P, uint64_t Pni, uint64_t R2, uint64_t omega, int N,
                                   int batch, const uint64_t* in, uint64_t* out, uint64_t scale) {
+  pdl_wait();
   const long long total = (long long)batch * N;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -203,8 +208,8 @@ int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64
   const uint64_t R2 = (uint64_t)(R * R % p);
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  dft_direct_kernel<<<(unsigned)blocks, 256, 0, st>>>(p, tmp.Pni, R2, omega, N, batch, in, out,
-                                                      scale);
+  FPM_CUDA_TRY(launch_pdl(dft_direct_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, tmp.Pni, R2, omega, N, batch, in, out,
+                                                      scale));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -236,7 +241,7 @@ int launch_crt(const CrtArgs& a, cudaStream_t st) {
   if (total <= 0) return kOk;
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  crt_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  FPM_CUDA_TRY(launch_pdl(crt_kernel, dim3((unsigned)blocks), dim3(256), 0, st, a));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -247,9 +252,9 @@ int launch_middle_entrywise(const MiddleEntryArgs& a, cudaStream_t st) {
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   if (a.in64 && a.out64)
-    middle_entrywise_kernel<uint64_t, uint64_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+    FPM_CUDA_TRY(launch_pdl(middle_entrywise_kernel<uint64_t, uint64_t>, dim3((unsigned)blocks), dim3(256), 0, st, a));
   else if (!a.in64 && !a.out64)
-    middle_entrywise_kernel<uint32_t, uint32_t><<<(unsigned)blocks, 256, 0, st>>>(a);
+    FPM_CUDA_TRY(launch_pdl(middle_entrywise_kernel<uint32_t, uint32_t>, dim3((unsigned)blocks), dim3(256), 0, st, a));
   else {
     set_last_error("middle_entrywise: mixed element widths unsupported");
     return kInvalidArgument;
@@ -264,9 +269,9 @@ int launch_max_len(const void* M, int in64, long long entries, int L, int* out, 
   long long blocks = (entries * 32 + 255) / 256;  // one warp per entry
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (in64)
-    max_len_kernel<uint64_t><<<(unsigned)blocks, 256, 0, st>>>((const uint64_t*)M, entries, L, out);
+    FPM_CUDA_TRY(launch_pdl(max_len_kernel<uint64_t>, dim3((unsigned)blocks), dim3(256), 0, st, (const uint64_t*)M, entries, L, out));
   else
-    max_len_kernel<uint32_t><<<(unsigned)blocks, 256, 0, st>>>((const uint32_t*)M, entries, L, out);
+    FPM_CUDA_TRY(launch_pdl(max_len_kernel<uint32_t>, dim3((unsigned)blocks), dim3(256), 0, st, (const uint32_t*)M, entries, L, out));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -277,9 +282,9 @@ int launch_rdeg(const void* M, int in64, int rows, int cols, int L, const int64_
   const int wpb = 8;
   const unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
   if (in64)
-    rdeg_kernel<uint64_t><<<blocks, wpb * 32, 0, st>>>((const uint64_t*)M, rows, cols, L, s, out);
+    FPM_CUDA_TRY(launch_pdl(rdeg_kernel<uint64_t>, dim3(blocks), dim3(wpb * 32), 0, st, (const uint64_t*)M, rows, cols, L, s, out));
   else
-    rdeg_kernel<uint32_t><<<blocks, wpb * 32, 0, st>>>((const uint32_t*)M, rows, cols, L, s, out);
+    FPM_CUDA_TRY(launch_pdl(rdeg_kernel<uint32_t>, dim3(blocks), dim3(wpb * 32), 0, st, (const uint32_t*)M, rows, cols, L, s, out));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

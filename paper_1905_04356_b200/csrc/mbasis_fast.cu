@@ -245,6 +245,7 @@ constexpr int kStepThreads = 512;
   if (a.trace && tid == 0) a.trace[k * 8 + (ev)] = clock64();
 
 __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __grid_constant__ StepArgs a) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
   const int m = a.m, n = a.n, T = a.T;
   const int tid = threadIdx.x;
@@ -649,6 +650,7 @@ struct BuildArgs {
 // them by x) and computes the kernel rows P1[t][klist[kr]] = P0[t][klist[kr]]
 // + sum_q Ct[q][kr] P0[t][plist[q]] with independent shared loads.
 __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
+  pdl_wait();
   extern __shared__ __align__(16) uint32_t bsm[];
   const int m = a.m, T = a.T, j = blockIdx.x;
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -827,7 +829,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   }
   {
     StageTimer t_(cx, "mbasis_steps");
-    mbasis_steps_kernel<<<1, kStepThreads, smem, cx.stream()>>>(sa);
+    FPM_CUDA_TRY(launch_pdl(mbasis_steps_kernel, dim3(1), dim3(kStepThreads), smem, cx.stream(), sa));
     FPM_LAUNCH_CHECK();
   }
   BuildArgs ba{};
@@ -842,7 +844,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   }
   {
     StageTimer t_(cx, "mbasis_build");
-    mbasis_build_kernel<<<m, 256, bsmem, cx.stream()>>>(ba);
+    FPM_CUDA_TRY(launch_pdl(mbasis_build_kernel, dim3(m), dim3(256), bsmem, cx.stream(), ba));
     FPM_LAUNCH_CHECK();
   }
   return kOk;

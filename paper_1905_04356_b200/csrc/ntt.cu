@@ -47,6 +47,7 @@ __device__ __forceinline__ uint32_t load_coef(const NttFwdArgs& a, const PrimeCo
 template <int LOGN, bool SINGLE, int TPCX>
 __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     ntt_fwd_kernel(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps) {
+  pdl_wait();
   using G = Geo<LOGN, TPCX>;
   extern __shared__ uint32_t sm[];
   const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
 template <int LOGN, bool SINGLE, int TPCX>
 __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS)
     ntt_inv_kernel(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps) {
+  pdl_wait();
   using G = Geo<LOGN, TPCX>;
   extern __shared__ uint32_t sm[];
   const PrimeConst& pc = ps.pr[SINGLE ? 0 : blockIdx.z];
@@ -320,7 +322,7 @@ int fwd_launch(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
     }
   }
   dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_fwd_kernel<LOGN, SINGLE, TPCX><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  FPM_CUDA_TRY(launch_pdl(ntt_fwd_kernel<LOGN, SINGLE, TPCX>, dim3(grid), dim3(G::THREADS), G::SMEM_BYTES, st, a, ps));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -359,7 +361,7 @@ int inv_launch(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
     }
   }
   dim3 grid((unsigned)((a.n_entries + G::TPC - 1) / G::TPC), 1, (unsigned)ps.count);
-  ntt_inv_kernel<LOGN, SINGLE, TPCX><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(a, ps);
+  FPM_CUDA_TRY(launch_pdl(ntt_inv_kernel<LOGN, SINGLE, TPCX>, dim3(grid), dim3(G::THREADS), G::SMEM_BYTES, st, a, ps));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

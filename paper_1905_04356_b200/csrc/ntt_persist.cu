@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   constexpr int FIRST = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
 
   stage_table<LOGN>(tws, pc.tw);
+  pdl_wait();  // constant tables above; data below may come from the previous kernel
+  pdl_trigger();
 
   uint32_t pre[32];
   auto load_group = [&](long long grp) {
@@ -281,6 +283,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   constexpr int GQ = G::TPC / PW;
 
   stage_table<LOGN>(tws, pc.itw);
+  pdl_wait();
+  pdl_trigger();
 
   uint32_t pre[32];
   auto load_group = [&](long long grp) {
@@ -446,9 +450,9 @@ int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
   if (grid > groups) grid = groups;
   dim3 g3((unsigned)grid, 1, (unsigned)ps.count);
   if constexpr (FWD)
-    ntt_fwd_persist<LOGN, SINGLE, TPCX><<<g3, G::THREADS, smem, st>>>(a, ps);
+    FPM_CUDA_TRY(launch_pdl(ntt_fwd_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps));
   else
-    ntt_inv_persist<LOGN, SINGLE, TPCX><<<g3, G::THREADS, smem, st>>>(a, ps);
+    FPM_CUDA_TRY(launch_pdl(ntt_inv_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

@@ -25,6 +25,7 @@ namespace {
 
 __global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* out,
                              long long out_stride, long long entries, int len) {
+  pdl_wait();
   const long long total = entries * len;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -39,6 +40,7 @@ __global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* 
 __global__ void split_reduce_kernel(const void* in, int in64, int reduce, long long stride,
                                     long long entries, int len, const __grid_constant__ PrimeSet ps,
                                     uint32_t* out) {
+  pdl_wait();
   const PrimeConst& pc = ps.pr[blockIdx.y];
   const long long total = entries * len;
   uint32_t* o = out + (long long)blockIdx.y * total;
@@ -54,6 +56,7 @@ __global__ void split_reduce_kernel(const void* in, int in64, int reduce, long l
 
 __global__ void zero_tail_kernel(void* out, int is64, long long stride, long long entries,
                                  int from, int to) {
+  pdl_wait();
   const int w = to - from;
   const long long total = entries * w;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -76,8 +79,8 @@ unsigned grid_for(long long total) {
 
 int zero_out(OutRef C, long long entries, int from, int to, cudaStream_t st) {
   if (to <= from || entries <= 0) return kOk;
-  zero_tail_kernel<<<grid_for(entries * (to - from)), 256, 0, st>>>(C.ptr, C.is64, C.stride,
-                                                                   entries, from, to);
+  FPM_CUDA_TRY(launch_pdl(zero_tail_kernel, dim3(grid_for(entries * (to - from))), dim3(256), 0, st, C.ptr, C.is64, C.stride,
+                                                                   entries, from, to));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -208,8 +211,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     uint32_t* buf;
     FPM_TRY(ws.get((size_t)r * entries * f.len, &buf));
     dim3 g((unsigned)grid_for(entries * f.len), (unsigned)r);
-    split_reduce_kernel<<<g, 256, 0, st>>>(f.in, f.in64, f.reduce, f.in_stride, entries, f.len,
-                                           ps, buf);
+    FPM_CUDA_TRY(launch_pdl(split_reduce_kernel, dim3(g), dim3(256), 0, st, f.in, f.in64, f.reduce, f.in_stride, entries, f.len,
+                                           ps, buf));
     FPM_LAUNCH_CHECK();
     f.in = buf; f.in64 = 0; f.reduce = 0; f.in_stride = f.len;
     f.in_prime_stride = entries * f.len;
@@ -313,8 +316,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     }
     StageTimer t2_(cx, direct ? "widen" : "crt");
     if (direct) {
-      widen_kernel<<<grid_for(ec * wlen), 256, 0, st>>>(R, wlen, (uint64_t*)C.ptr, C.stride,
-                                                      ec, wlen);
+      FPM_CUDA_TRY(launch_pdl(widen_kernel, dim3(grid_for(ec * wlen)), dim3(256), 0, st, R, wlen, (uint64_t*)C.ptr, C.stride,
+                                                      ec, wlen));
       FPM_LAUNCH_CHECK();
     } else {
       CrtArgs ca{};

@@ -99,6 +99,7 @@ constexpr int kLeafThreads = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(kLeafThreads) mbasis_leaf_kernel(LeafArgs<T> a) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smraw[];
   const int m = a.m, n = a.n;
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -295,7 +296,7 @@ int launch_leaf(Context& cx, uint64_t p, const void* F, int m, int n, long long 
   if (smem > 48 * 1024)
     FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_leaf_kernel<T>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  mbasis_leaf_kernel<T><<<1, kLeafThreads, smem, cx.stream()>>>(la);
+  FPM_CUDA_TRY(launch_pdl(mbasis_leaf_kernel<T>, dim3(1), dim3(kLeafThreads), smem, cx.stream(), la));
   FPM_LAUNCH_CHECK();
   // the pooled Pa/Pb return to the pool; stream order keeps reuse safe
   return kOk;

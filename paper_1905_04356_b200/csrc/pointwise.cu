@@ -31,6 +31,7 @@ template <int K, int WR, int WC>
 __global__ void __launch_bounds__(WR * WC * 32, 1)
     pointwise_cc_kernel(const __grid_constant__ PointwiseArgs a,
                         const __grid_constant__ PrimeSet ps, int tiles_n) {
+  pdl_wait();
   constexpr int wr = WR, wc = WC, nthreads = WR * WC * 32;
   extern __shared__ __align__(16) uint32_t sm[];
   const PrimeConst& pc = ps.pr[blockIdx.z];
@@ -138,7 +139,7 @@ int launch_t(const PointwiseArgs& a, const PrimeSet& ps, cudaStream_t st) {
     attr = true;
   }
   dim3 grid((unsigned)a.nblk, (unsigned)(tiles_m * tiles_n), (unsigned)ps.count);
-  pointwise_cc_kernel<K, WR, WC><<<grid, WR * WC * 32, smem, st>>>(a, ps, tiles_n);
+  FPM_CUDA_TRY(launch_pdl(pointwise_cc_kernel<K, WR, WC>, dim3(grid), dim3(WR * WC * 32), smem, st, a, ps, tiles_n));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

@@ -1,5 +1,6 @@
 // runtime.cu -- context, allocator, plan cache, error string, host number theory.
 #include "runtime.cuh"
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -267,6 +268,11 @@ int Context::profile_get(int i, const char** name, float* ms) {
   FPM_CUDA_TRY(cudaEventElapsedTime(ms, stages_[i].a, stages_[i].b));
   *name = stages_[i].name;
   return kOk;
+}
+
+bool pdl_enabled() {
+  static const bool on = std::getenv("FPM_NO_PDL") == nullptr;
+  return on;
 }
 
 int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {

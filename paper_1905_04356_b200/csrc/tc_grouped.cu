@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  pdl_wait();  // operands come from the forward transforms
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
@@ -353,7 +354,7 @@ int launch_nb(const CUtensorMap& mA, const CUtensorMap& mB, const GArgs& a, cons
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr = true;
   }
-  tc_grouped_kernel<NB><<<grid, kThreads, kSmem, st>>>(mA, mB, a, ps);
+  FPM_CUDA_TRY(launch_pdl(tc_grouped_kernel<NB>, dim3(grid), dim3(kThreads), kSmem, st, mA, mB, a, ps));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

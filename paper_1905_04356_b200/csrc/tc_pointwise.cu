@@ -48,6 +48,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool o
 
 __global__ void __launch_bounds__(kThreads, 1)
     tc_pointwise_kernel(const __grid_constant__ TcArgs a, const __grid_constant__ PrimeSet ps) {
+  pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t mbar[NSTAGE];
   __shared__ uint32_t tmem_base;
@@ -231,7 +232,7 @@ int launch_tc_pointwise(const TcArgs& a, const PrimeSet& ps, cudaStream_t st) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const long long grid = items < sms ? items : sms;
-  tc_pointwise_kernel<<<(unsigned)grid, kThreads, kSmem, st>>>(a, ps);
+  FPM_CUDA_TRY(launch_pdl(tc_pointwise_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, a, ps));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

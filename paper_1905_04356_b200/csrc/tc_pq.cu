@@ -190,6 +190,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
+  pdl_wait();  // operands come from the forward transforms
+  pdl_trigger();
   const uint32_t tmem = tmem_base;
   const int nq = G / 4;  // point quads per item
 
@@ -512,8 +514,8 @@ int launch_nb(const CUtensorMap& mA, const CUtensorMap& mB, const QArgs& a, cons
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr = true;
   }
-  tc_pq_kernel<NB><<<grid, kThreads, kSmem, st>>>(mA, mB, a, ps);
-  const cudaError_t err = cudaGetLastError();
+  const cudaError_t lerr = launch_pdl(tc_pq_kernel<NB>, dim3(grid), dim3(kThreads), kSmem, st, mA, mB, a, ps);
+  const cudaError_t err = lerr != cudaSuccess ? lerr : cudaGetLastError();
   if (err != cudaSuccess) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, tc_pq_kernel<NB>);
