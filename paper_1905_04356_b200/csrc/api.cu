@@ -170,6 +170,12 @@ int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, 
   return polmat_mul(*ctx->cx, p, m, k, n, Ar, Br, Cr);
 }
 
+// Host-buffer product.  Large products are pipelined over R x R blocks of C:
+// the copy-in stream uploads A's row blocks and B's column blocks in the order
+// the blocks need them, the context stream multiplies block (i, j) as soon as
+// A_i and B_j have landed, and the copy-out stream downloads C_ij while later
+// blocks compute and upload -- PCIe traffic in both directions overlaps itself
+// and the kernels instead of running as three serial phases.
 int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
                         int k, int la, const void* B, int n, int lb, void* C) {
   if (!ctx) return kInvalidArgument;
@@ -185,12 +191,96 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   FPM_TRY(ws.get(esz * na + 1, &dA));
   FPM_TRY(ws.get(esz * nb + 1, &dB));
   FPM_TRY(ws.get(esz * nc + 1, &dC));
-  if (na) FPM_CUDA_TRY(cudaMemcpyAsync(dA, A, esz * na, cudaMemcpyHostToDevice, cx.stream()));
-  if (nb) FPM_CUDA_TRY(cudaMemcpyAsync(dB, B, esz * nb, cudaMemcpyHostToDevice, cx.stream()));
-  FPM_TRY(fpm_polmat_mul(ctx, p, elem_bytes, dA, m, k, la, dB, n, lb, dC));
-  if (nc) FPM_CUDA_TRY(cudaMemcpyAsync(C, dC, esz * nc, cudaMemcpyDeviceToHost, cx.stream()));
-  FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
-  return kOk;
+  static const int force = std::getenv("FPM_HOST_BLOCKS") ? std::atoi(std::getenv("FPM_HOST_BLOCKS")) : 0;
+  int R = force > 0 ? force : (esz * nc >= (256u << 20) ? 4 : esz * nc >= (8u << 20) ? 2 : 1);
+  if (R > m) R = m;
+  if (R > n) R = n;
+  if (R <= 1 || lc == 0) {
+    if (na) FPM_CUDA_TRY(cudaMemcpyAsync(dA, A, esz * na, cudaMemcpyHostToDevice, cx.stream()));
+    if (nb) FPM_CUDA_TRY(cudaMemcpyAsync(dB, B, esz * nb, cudaMemcpyHostToDevice, cx.stream()));
+    FPM_TRY(fpm_polmat_mul(ctx, p, elem_bytes, dA, m, k, la, dB, n, lb, dC));
+    if (nc) FPM_CUDA_TRY(cudaMemcpyAsync(C, dC, esz * nc, cudaMemcpyDeviceToHost, cx.stream()));
+    FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
+    return kOk;
+  }
+  cudaStream_t up, down;
+  FPM_TRY(cx.aux_stream(0, &up));
+  FPM_TRY(cx.aux_stream(1, &down));
+  const cudaStream_t st = cx.stream();
+  auto lo = [&](int i, int tot) { return (int)((long long)tot * i / R); };
+  std::vector<cudaEvent_t> evs;
+  auto ev = [&]() {
+    cudaEvent_t e = cx.take_event();
+    evs.push_back(e);
+    return e;
+  };
+  int status = kOk;
+  auto fail = [&](cudaError_t e) {
+    if (e != cudaSuccess && status == kOk) {
+      set_last_error("pipelined host product: %s", cudaGetErrorString(e));
+      status = kCudaError;
+    }
+  };
+  {
+    cudaEvent_t start = ev();  // buffers were last used in the context stream's order
+    fail(cudaEventRecord(start, st));
+    fail(cudaStreamWaitEvent(up, start, 0));
+    fail(cudaStreamWaitEvent(down, start, 0));
+  }
+  const int is64 = elem_bytes == 8;
+  std::vector<bool> a_up(R, false), b_up(R, false);
+  // each row block of A and column block of B is transformed once and its
+  // evaluations reused by the other blocks of its row / column
+  std::vector<EvalCache> ca(R), cb(R);
+  for (int i = 0; i < R && status == kOk; ++i) {
+    const int i0 = lo(i, m), i1 = lo(i + 1, m), ib = i1 - i0;
+    for (int j = 0; j < R && status == kOk; ++j) {
+      const int j0 = lo(j, n), j1 = lo(j + 1, n), jb = j1 - j0;
+      unsigned char* dAi = dA + esz * (size_t)i0 * k * la;
+      unsigned char* dBj = dB + esz * (size_t)k * j0 * lb;  // column block j, packed [k][jb][lb]
+      unsigned char* dCij = dC + esz * ((size_t)i0 * n + (size_t)ib * j0) * lc;  // packed [ib][jb][lc]
+      if (!a_up[i]) {
+        fail(cudaMemcpyAsync(dAi, (const unsigned char*)A + esz * (size_t)i0 * k * la,
+                             esz * (size_t)ib * k * la, cudaMemcpyHostToDevice, up));
+        a_up[i] = true;
+      }
+      if (!b_up[j]) {
+        fail(cudaMemcpy2DAsync(dBj, esz * (size_t)jb * lb,
+                               (const unsigned char*)B + esz * (size_t)j0 * lb, esz * (size_t)n * lb,
+                               esz * (size_t)jb * lb, k, cudaMemcpyHostToDevice, up));
+        b_up[j] = true;
+      }
+      cudaEvent_t landed = ev();
+      fail(cudaEventRecord(landed, up));
+      fail(cudaStreamWaitEvent(st, landed, 0));
+      if (status != kOk) break;
+      MatRef Ar{dAi, is64, la, la};
+      MatRef Br{dBj, is64, lb, lb};
+      OutRef Cr{dCij, is64, lc, lc};
+      const int s2 = polmat_mul_cached(cx, p, ib, k, jb, Ar, Br, Cr, &ca[i], &cb[j]);
+      if (s2 != kOk) {
+        status = s2;
+        break;
+      }
+      cudaEvent_t done = ev();
+      fail(cudaEventRecord(done, st));
+      fail(cudaStreamWaitEvent(down, done, 0));
+      fail(cudaMemcpy2DAsync((unsigned char*)C + esz * ((size_t)i0 * n + j0) * lc,
+                             esz * (size_t)n * lc, dCij, esz * (size_t)jb * lc,
+                             esz * (size_t)jb * lc, ib, cudaMemcpyDeviceToHost, down));
+    }
+  }
+  // the workspace returns to the pool in the context stream's order
+  cudaEvent_t fin = ev();
+  fail(cudaEventRecord(fin, down));
+  fail(cudaStreamWaitEvent(st, fin, 0));
+  fail(cudaStreamSynchronize(st));
+  for (auto e : evs) cx.give_event(e);
+  for (auto& c : ca)
+    if (c.EA) cx.release(c.EA);
+  for (auto& c : cb)
+    if (c.EA) cx.release(c.EA);
+  return status;
 }
 
 struct fpm_multiplier {

@@ -108,7 +108,7 @@ int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L
 }
 
 int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
-                   int logn, long long off, OutRef C, EvalCache* cache) {
+                   int logn, long long off, OutRef C, EvalCache* cache, EvalCache* cache_b) {
   cudaStream_t st = cx.stream();
   const long long ec = (long long)m * n;
   if (ec == 0 || C.len <= 0) return kOk;
@@ -160,9 +160,9 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // ---- workspaces ------------------------------------------------------------
   Workspace ws(cx);
   const long long ea = (long long)m * k, eb = (long long)k * n;
-  uint32_t *EA = nullptr, *EB, *EC;
+  uint32_t *EA = nullptr, *EB = nullptr, *EC;
   if (!cache) FPM_TRY(ws.get(r * N * ea, &EA));
-  FPM_TRY(ws.get(r * N * eb, &EB));
+  if (!cache_b || fold) FPM_TRY(ws.get(r * N * eb, &EB));
   FPM_TRY(ws.get(r * N * ec, &EC));
 
   const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
@@ -218,42 +218,57 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     f.in_prime_stride = entries * f.len;
     return kOk;
   };
-  FPM_TRY(to_u32(fb, eb));
-  bool a_cached = false;
-  if (cache) {
+  // cached evaluations (Multiplier; blocked host pipeline): an operand whose
+  // transforms are already in its cache for this exact plan is not transformed
+  auto bind = [&](EvalCache* c, int rows, int cols, int len, long long entries, uint32_t** E,
+                  bool* hit) -> int {
     const int pm_now = use_tc ? 1 : 0, pl_now = pq ? 2 : 5;
-    bool match = cache->valid && cache->p == p && cache->m == m && cache->k == k &&
-                 cache->a_len == A.len && cache->logn == logn && cache->r == r &&
-                 cache->pm == pm_now && cache->pblk_log == pl_now;
-    for (int i = 0; i < r && match; ++i) match = cache->primes[i] == primes[i];
-    const size_t words = (size_t)r * N * ea;
+    bool match = c->valid && c->p == p && c->m == rows && c->k == cols && c->a_len == len &&
+                 c->logn == logn && c->r == r && c->pm == pm_now && c->pblk_log == pl_now;
+    for (int i = 0; i < r && match; ++i) match = c->primes[i] == primes[i];
+    const size_t words = (size_t)r * N * entries;
     if (!match) {
-      if (cache->EA && cache->words < words) {
-        cx.release(cache->EA);
-        cache->EA = nullptr;
+      if (c->EA && c->words < words) {
+        cx.release(c->EA);
+        c->EA = nullptr;
       }
-      if (!cache->EA) {
+      if (!c->EA) {
         void* ptr = nullptr;
         FPM_TRY(cx.alloc(words * 4, &ptr));
-        cache->EA = (uint32_t*)ptr;
-        cache->words = words;
+        c->EA = (uint32_t*)ptr;
+        c->words = words;
       }
-      cache->valid = false;
-      cache->p = p; cache->m = m; cache->k = k; cache->a_len = A.len; cache->logn = logn;
-      cache->r = r; cache->pm = pm_now; cache->pblk_log = pl_now;
-      for (int i = 0; i < r; ++i) cache->primes[i] = primes[i];
+      c->valid = false;
+      c->p = p; c->m = rows; c->k = cols; c->a_len = len; c->logn = logn;
+      c->r = r; c->pm = pm_now; c->pblk_log = pl_now;
+      for (int i = 0; i < r; ++i) c->primes[i] = primes[i];
     }
-    EA = cache->EA;
+    *E = c->EA;
+    *hit = match;
+    return kOk;
+  };
+  bool a_cached = false, b_cached = false;
+  if (cache) {
+    FPM_TRY(bind(cache, m, k, A.len, ea, &EA, &a_cached));
     fa.out = EA;
-    a_cached = match;
   }
+  if (cache_b && !fold) {
+    FPM_TRY(bind(cache_b, k, n, B.len, eb, &EB, &b_cached));
+    fb.out = EB;
+  }
+  if (!b_cached) FPM_TRY(to_u32(fb, eb));
   // both operands in one launch when their transforms are alike (persistent
   // grid: one tail wave instead of two)
   static const bool no_pair = std::getenv("FPM_NTT_NO_PAIR") != nullptr;
   if (!a_cached) FPM_TRY(to_u32(fa, ea));
-  if (a_cached) {
+  if (a_cached && b_cached) {
+    // both evaluations reused
+  } else if (a_cached) {
     StageTimer t_(cx, "ntt_fwd_B");
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
+  } else if (b_cached) {
+    StageTimer t_(cx, "ntt_fwd_A");
+    FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
   } else if (!no_pair && fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
              fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
     NttFwdArgs fab = fa;
@@ -270,6 +285,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     FPM_TRY(launch_ntt_fwd(logn, fb, ps, st));
   }
 
+  if (cache_b && !fold) cache_b->valid = true;
   if (cache) cache->valid = true;  // A's evaluations are in place (stream order)
 
   if (pq) {
@@ -332,11 +348,16 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
 }
 
 int polmat_mul(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B, OutRef C) {
+  return polmat_mul_cached(cx, p, m, k, n, A, B, C, nullptr, nullptr);
+}
+
+int polmat_mul_cached(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                      OutRef C, EvalCache* ca, EvalCache* cb) {
   if (A.len <= 0 || B.len <= 0 || k == 0)
     return zero_out(C, (long long)m * n, 0, C.len, cx.stream());
   const long long need = (long long)A.len + B.len - 1;
   const int logn = ceil_log2_min1(need);
-  return cyclic_product(cx, p, m, k, n, A, B, logn, 0, C);
+  return cyclic_product(cx, p, m, k, n, A, B, logn, 0, C, ca, cb);
 }
 
 int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,

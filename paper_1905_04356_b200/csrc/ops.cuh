@@ -41,9 +41,15 @@ struct EvalCache {
 // C = window of (A * fold_N(B)) mod (x^N - 1) over F_p:
 //   C[e][t] = cyc[(off + t) mod N], t < out.len, N = 2^logn.
 // With N >= len(A) + len(B) - 1 and no fold this is the plain product.
-// With `cache`, A's forward transforms are taken from / stored into it.
+// With `cache` (`cache_b`), A's (B's) forward transforms are taken from /
+// stored into it.
 int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
-                   int logn, long long off, OutRef C, EvalCache* cache = nullptr);
+                   int logn, long long off, OutRef C, EvalCache* cache = nullptr,
+                   EvalCache* cache_b = nullptr);
+
+// product with optional evaluation caches for either factor (host pipeline)
+int polmat_mul_cached(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
+                      OutRef C, EvalCache* ca, EvalCache* cb);
 
 // full product A*B (length la + lb - 1, truncated/padded to C.len)
 int polmat_mul(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B, OutRef C);

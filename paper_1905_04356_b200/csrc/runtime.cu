@@ -92,6 +92,9 @@ Context::~Context() {
     cudaFree(kv.second.itw_s);
   }
   if (pinned_) cudaFreeHost(pinned_);
+  for (auto& a : aux_)
+    if (a) cudaStreamDestroy(a);
+  for (auto e : ev_pool_) cudaEventDestroy(e);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
 }
 
@@ -268,6 +271,30 @@ int Context::profile_get(int i, const char** name, float* ms) {
   FPM_CUDA_TRY(cudaEventElapsedTime(ms, stages_[i].a, stages_[i].b));
   *name = stages_[i].name;
   return kOk;
+}
+
+int Context::aux_stream(int i, cudaStream_t* out) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!aux_[i]) FPM_CUDA_TRY(cudaStreamCreateWithFlags(&aux_[i], cudaStreamNonBlocking));
+  *out = aux_[i];
+  return kOk;
+}
+
+cudaEvent_t Context::take_event() {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!ev_pool_.empty()) {
+    cudaEvent_t e = ev_pool_.back();
+    ev_pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+void Context::give_event(cudaEvent_t e) {
+  std::lock_guard<std::mutex> lk(mu_);
+  ev_pool_.push_back(e);
 }
 
 bool pdl_enabled() {

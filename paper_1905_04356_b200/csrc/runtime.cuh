@@ -35,6 +35,11 @@ class Context {
   int pinned(size_t bytes, void** out);
 
   int plan(uint32_t p, int logn, const Plan** out);
+
+  // copy streams of the pipelined host entry points (created on first use)
+  int aux_stream(int i, cudaStream_t* out);
+  cudaEvent_t take_event();
+  void give_event(cudaEvent_t e);
   int prime_const(uint32_t p, int logn, PrimeConst* out);
 
   // stage profiling (tracing subsystem): CUDA events around each kernel
@@ -57,6 +62,8 @@ class Context {
   int device_;
   cudaStream_t stream_ = nullptr;
   bool own_stream_ = false;
+  cudaStream_t aux_[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_pool_;
   std::mutex mu_;
   std::multimap<size_t, void*> free_;
   std::map<void*, size_t> used_;
