@@ -171,6 +171,20 @@ def read_traffic():
         return {}
 
 
+def read_pipes():
+    path = os.path.join(ROOT, "profiles", "ncu_pipes.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# measured issue cost of the integer multiply forms on this B200
+# (tools/micro/tput.cu: cycles per warp-instruction per SM sub-partition)
+INT_RATES = {"imad": 2.0, "imad_hi": 4.45, "imad_wide": 4.0, "iadd": 1.0, "viaddmnmx": 2.0}
+
+
 # ---------------------------------------------------------------------------
 def read_int8_peak():
     """Measured int8 tensor-core peak (tools/int8_peak.py on this pool's B200:
@@ -265,8 +279,25 @@ def roofline_report(cfg, cfgname, avg, sbytes):
             "traffic": sum(trs) if all(t is not None for t in trs) else None,
             "algorithmic_bytes": b, "ms": round(ms, 5), "peak_source": hsrc}
     if dom == "ntt":
-        roof["note"] = ("HBM fraction per SURVEY 8(d); the NTT kernels are integer-ALU/issue "
-                        "bound (~7 instructions per butterfly), see DESIGN.md")
+        roof["note"] = ("HBM fraction per SURVEY 8(d).  The NTT kernels are bound by the "
+                        "integer multiply path, not HBM: every Shoup modmul issues one IMAD.HI "
+                        "(quarter rate, 4.45 cycles/warp-op/SMSP measured) and two IMAD on the "
+                        "heavy FMA pipe; `compute` gives ncu pipe/issue utilisation, DESIGN.md 4")
+        pipes = read_pipes().get(cfgname, {})
+        comp = {}
+        for st in ("ntt_fwd", "ntt_inv"):
+            ent = pipes.get(st)
+            if ent:
+                e = ent[0]
+                comp[st] = {"kernel": e["kernel"], "fmaheavy_util_elapsed": e["fmaheavy_pct_elapsed"],
+                            "alu_util_elapsed": e["alu_pct_elapsed"],
+                            "issue_util_active": e["issue_pct_active"]}
+        if comp:
+            roof["compute"] = {"pipe": "fmaheavy (IMAD.HI / IMAD, Shoup butterflies)",
+                               "per_kernel": comp,
+                               "int_rates_cycles_per_warp_op": INT_RATES,
+                               "source": "profiles/ncu_pipes.json (ncu --set full), "
+                                         "tools/micro/tput.cu"}
     if dom == "pointwise" and "pointwise_tc" in table and "tensor" in table["pointwise_tc"]:
         t = table["pointwise_tc"]["tensor"]
         roof.update({"bound": "tensor", "achieved": t["issued_tops"], "peak": i8,

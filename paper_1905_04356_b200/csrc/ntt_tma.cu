@@ -82,10 +82,6 @@ struct TmaFwdArgs {
   int in_words;  // input buffer words: N/2 (upper half zero) or N
   int pl;        // eval block log: 5 (E[N/32][e][32]) or 2 (E[N/4][e][4])
   int diag;      // FPM_NTT_DIAG bit 0: skip the output stores (timing experiments only)
-  int direct;    // PL = 2: chunks 0 .. direct-1 stored from registers (LSU), the rest by TMA
-  uint32_t* out1;
-  uint32_t* out2;
-  long long out1_ps, out2_ps;
 };
 
 struct TmaInvArgs {
@@ -280,24 +276,14 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
     // pass 3: thread lt ends with points 32 lt .. 32 lt + 31
     from_smem<LOGN, MAP_LAST>(tile, v, lt);
     dit_lazy<T::LAST_R, true, false>(v, pc.w32, p);
+    // (the 16-byte quad pieces could also leave through the LSU: measured
+    // slower than the TMA unit alone, so every chunk is staged)
     const bool second = item >= a.n1;
-    if constexpr (PL == 2) {
-      // the quad layout scatters 16-byte pieces: split them between the LSU
-      // (direct stores of the first chunks) and the TMA unit (the rest)
-      uint32_t* ob = second ? a.out2 + z * a.out2_ps : a.out1 + z * a.out1_ps;
-      const long long ne = second ? a.n2 : a.n1, e = second ? item - a.n1 : item;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < a.direct)
-          *reinterpret_cast<uint4*>(ob + (((long long)(8 * lt + c)) * ne + e) * 4) =
-              make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
-    }
     gsync(bar, T::TPT);  // every padded read done before dense rows overwrite the tile
 #pragma unroll
     for (int c = 0; c < 8; ++c)
-      if (PL == 5 || c >= a.direct)
-        *reinterpret_cast<uint4*>(tile8 + chunk_off<LOGN, PL>(lt, c)) =
-            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      *reinterpret_cast<uint4*>(tile8 + chunk_off<LOGN, PL>(lt, c)) =
+          make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     tc::fence_proxy_async();
     gsync(bar, T::TPT);
     if (leader && !(a.diag & 1)) {
@@ -307,8 +293,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
         tma_store_4d(om, tile_s, 0, e, 0, z);
       } else {
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          if (c >= a.direct) tma_store_5d(om, tile_s + c * (T::N / 2), 0, e, c, 0, z);
+        for (int c = 0; c < 8; ++c) tma_store_5d(om, tile_s + c * (T::N / 2), 0, e, c, 0, z);
       }
       bulk_commit();
     }
@@ -538,10 +523,6 @@ int fwd_launch(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t st) {
   a.pl = f.pblk_log ? f.pblk_log : 5;
   static const int diag = std::getenv("FPM_NTT_DIAG") ? std::atoi(std::getenv("FPM_NTT_DIAG")) : 0;
   a.diag = diag;
-  static const int direct = std::getenv("FPM_NTT_DIRECT") ? std::atoi(std::getenv("FPM_NTT_DIRECT")) : 0;
-  a.direct = direct;
-  a.out1 = f.out; a.out1_ps = f.out_prime_stride;
-  a.out2 = two ? f.out2 : f.out; a.out2_ps = two ? f.out2_prime_stride : f.out_prime_stride;
   CUtensorMap m1, m2;
   FPM_TRY(make_eval_map(&m1, f.out, f.n_entries, T::N, a.pl, f.out_prime_stride, ps.count));
   if (two)

@@ -28,6 +28,11 @@ METRICS = [
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
     "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    # the integer multiply path: IMAD.HI / IMAD.WIDE issue at a quarter of the
+    # IMAD rate on the heavy FMA pipe (tools/micro/tput.cu)
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_elapsed",
 ]
 
 STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_inv": "ntt_inv", "pointwise_cc": "pointwise",
@@ -103,6 +108,23 @@ def full(path, key=None):
                 b = rec["dram__bytes_read.sum"] + rec.get("dram__bytes_write.sum", 0.0)
                 ent.setdefault(stage, []).append(b)
         json.dump(cur, open(tp, "w"), indent=1)
+        pp = os.path.join(ROOT, "profiles", "ncu_pipes.json")
+        cur = json.load(open(pp)) if os.path.exists(pp) else {}
+        ent = cur[key] = {}
+        for rec in res:
+            stage = next((v for k, v in STAGE_OF.items() if k in rec["kernel"]), None)
+            if not stage:
+                continue
+            ent.setdefault(stage, []).append({
+                "kernel": rec["kernel"],
+                "us": rec.get("gpu__time_duration.sum"),
+                "fmaheavy_pct_elapsed": rec.get(
+                    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "alu_pct_elapsed": rec.get("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+                "issue_pct_elapsed": rec.get("smsp__issue_active.avg.pct_of_peak_sustained_elapsed"),
+                "issue_pct_active": rec.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            })
+        json.dump(cur, open(pp, "w"), indent=1)
 
 
 if __name__ == "__main__":
