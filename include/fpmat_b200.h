@@ -140,6 +140,26 @@ int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes,
 /* base-case threshold used by fpm_pmbasis (default 32, config.py:18) */
 int fpm_set_pmbasis_threshold(fpm_context* ctx, int T);
 
+/* ---- interchange formats (polmat.polmat_to_text / polmat_from_text,
+ *      polmat.py:617-647) -- host code, all host threads --------------------
+ * Text is the reference's CLI format byte for byte: header "p m n", one line
+ * per entry (row-major), trimmed coefficients low degree first separated by
+ * one space, empty line for the zero polynomial, final newline.  M is a dense
+ * host matrix m x n x L (elem_bytes 4 or 8, entries trimmed on output).
+ * Reading follows polmat_from_text: str.splitlines() / str.split()
+ * semantics, integer tokens of any size reduced with Python's `% p`, missing
+ * lines are zero entries; FPM_ERR_INVALID_ARGUMENT (ValueError) for an empty
+ * text, a header that is not three integers or a non-integer token. */
+int fpm_polmat_text_size(uint64_t p, int elem_bytes, const void* M_host, int m, int n, int L,
+                         size_t* bytes);
+int fpm_polmat_to_text(uint64_t p, int elem_bytes, const void* M_host, int m, int n, int L,
+                       char* out, size_t cap, size_t* written);
+/* header and the longest entry after reduction and trimming */
+int fpm_polmat_text_dims(const char* text, size_t len, long long* p, int* m, int* n,
+                         int* max_len);
+/* dense m x n x L host output, zero-padded */
+int fpm_polmat_from_text(const char* text, size_t len, int elem_bytes, void* M_host, int L);
+
 /* ---- tracing: per-stage device time (CUDA events on the context stream) --
  * enable (clears previous records), run calls, then read stage i's name and
  * milliseconds (synchronizes on that stage). */

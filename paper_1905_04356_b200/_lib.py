@@ -91,6 +91,13 @@ def lib():
                                             ctypes.POINTER(vp)]),
             "fpm_multiplier_apply": (i32, [vp, vp, i32, i32, vp]),
             "fpm_multiplier_destroy": (None, [vp]),
+            "fpm_polmat_text_size": (i32, [u64, i32, vp, i32, i32, i32,
+                                           ctypes.POINTER(ctypes.c_size_t)]),
+            "fpm_polmat_to_text": (i32, [u64, i32, vp, i32, i32, i32, vp,
+                                         ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+            "fpm_polmat_text_dims": (i32, [ctypes.c_char_p, ctypes.c_size_t,
+                                           ctypes.POINTER(ctypes.c_longlong), pint, pint, pint]),
+            "fpm_polmat_from_text": (i32, [ctypes.c_char_p, ctypes.c_size_t, i32, vp, i32]),
             "fpm_profile_enable": (i32, [vp, i32]),
             "fpm_profile_count": (i32, [vp]),
             "fpm_profile_get": (i32, [vp, i32, ctypes.c_char_p, i32,
