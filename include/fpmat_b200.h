@@ -45,6 +45,7 @@ extern "C" {
 #define FPM_ERR_LENGTH_MISMATCH 7     /* errors.LengthMismatch  (modring.py:274-275) */
 #define FPM_ERR_OUT_OF_RANGE 8        /* errors.OutOfRange      (modring.py:157-158) */
 #define FPM_ERR_COMPOSITE_MODULUS 9   /* errors.CompositeModulus (modring.py:159-160) */
+#define FPM_ERR_DUPLICATE_POINTS 10   /* errors.DuplicatePoints (appint.py:203-205) */
 #define FPM_ERR_INVALID_ARGUMENT 20   /* ValueError */
 #define FPM_ERR_UNSUPPORTED 21        /* size outside the implemented kernels */
 #define FPM_ERR_CUDA 30
@@ -137,6 +138,27 @@ int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes,
 int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes,
                      const void* F_host, int m, int n, int lf, int order,
                      const int64_t* shift, void* P_host, int* lp, int64_t* rdeg_out);
+/* ---- interpolant bases (appint.m_intbasis / pm_intbasis,
+ *      appint.py:208-319) --------------------------------------------------
+ * E_dev: order constant matrices m x n, point-major [order][m][n]; alpha:
+ * order host points (reduced mod p, pairwise distinct, else
+ * FPM_ERR_DUPLICATE_POINTS); shift: m int64 (host).  P_dev receives the
+ * m x m s-ordered weak Popov interpolant basis with room for order+1
+ * coefficients; *lp = deg(P)+1; rdeg_out (host, optional) = rdeg_s(P).
+ * Pivot rows are multiplied by (x - alpha_k) (appint.py:79-117); the output
+ * is the reference's for every base threshold.  31-bit primes only
+ * (FPM_ERR_UNSUPPORTED otherwise), elem_bytes = 4. */
+int fpm_pm_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E_dev, int m,
+                    int n, int order, const uint64_t* alpha, const int64_t* shift,
+                    void* P_dev, int* lp, int64_t* rdeg_out);
+int fpm_m_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E_dev, int m,
+                   int n, int order, const uint64_t* alpha, const int64_t* shift,
+                   void* P_dev, int* lp, int64_t* rdeg_out);
+/* eval_polmat_points (appint.py:262-287): out_dev[t][i][j] = P_ij(pts[t]),
+ * P_dev m x n of length L; npts host points; 31-bit primes, elem_bytes 4. */
+int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const void* P_dev,
+                           int m, int n, int L, const uint64_t* pts, int npts, void* out_dev);
+
 /* base-case threshold used by fpm_pmbasis (default 32, config.py:18) */
 int fpm_set_pmbasis_threshold(fpm_context* ctx, int T);
 

@@ -2,7 +2,7 @@
 
 Drop-in for the hot path of the reference `fpmat` package (arXiv:1905.04356):
 ``pm_mul``, ``pm_middle_product`` / ``_pm_middle``, ``Multiplier``,
-``mbasis`` / ``pmbasis`` with the reference's names, argument meaning and
+``mbasis`` / ``pmbasis``, ``m_intbasis`` / ``pm_intbasis`` with the reference's names, argument meaning and
 exceptions, computed by hand-written sm_100a kernels in libfpm_b200.so
 (csrc/) behind the C ABI declared in include/fpmat_b200.h.
 """
@@ -20,11 +20,12 @@ from .polmat import (  # noqa: F401
     polmat_to_text,
     random_polmat,
 )
-from .appint import mbasis, mbasis1, pmbasis  # noqa: F401
+from .appint import eval_polmat_points, m_intbasis, mbasis, mbasis1, pm_intbasis, pmbasis  # noqa: F401
 from . import fraction, kernel  # noqa: F401,E402  (callers one level up)
 
 __all__ = [
     "FieldCtx", "NttPlan", "field_new", "cached_field", "ntt_forward", "ntt_inverse",
     "PolMat", "pm_mul", "pm_middle_product", "applicable_strategies", "Multiplier",
     "polmat_to_text", "polmat_from_text", "random_polmat", "mbasis", "mbasis1", "pmbasis",
+    "m_intbasis", "pm_intbasis", "eval_polmat_points",
 ]

@@ -34,6 +34,7 @@ _STATUS = {
     7: errors.LengthMismatch,
     8: errors.OutOfRange,
     9: errors.CompositeModulus,
+    10: errors.DuplicatePoints,
     20: ValueError,
     21: NotImplementedError,
 }
@@ -87,6 +88,12 @@ def lib():
             "fpm_pmbasis_host": (i32, [vp, u64, i32, vp, i32, i32, i32, i32, pi64, vp, pint,
                                        pi64]),
             "fpm_set_pmbasis_threshold": (i32, [vp, i32]),
+            "fpm_pm_intbasis": (i32, [vp, u64, i32, vp, i32, i32, i32,
+                                      ctypes.POINTER(ctypes.c_uint64), pi64, vp, pint, pi64]),
+            "fpm_m_intbasis": (i32, [vp, u64, i32, vp, i32, i32, i32,
+                                     ctypes.POINTER(ctypes.c_uint64), pi64, vp, pint, pi64]),
+            "fpm_polmat_eval_points": (i32, [vp, u64, i32, vp, i32, i32, i32,
+                                             ctypes.POINTER(ctypes.c_uint64), i32, vp]),
             "fpm_multiplier_create": (i32, [vp, u64, i32, vp, i32, i32, i32, i32,
                                             ctypes.POINTER(vp)]),
             "fpm_multiplier_apply": (i32, [vp, vp, i32, i32, vp]),

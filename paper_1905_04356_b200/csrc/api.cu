@@ -449,6 +449,41 @@ int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F
   return kOk;
 }
 
+int fpm_pm_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E, int m, int n,
+                    int order, const uint64_t* alpha, const int64_t* shift, void* P, int* lp,
+                    int64_t* rdeg_out) {
+  if (!ctx || !lp || (m > 0 && !shift) || (order > 0 && (!alpha || !E))) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (m <= 0 || n < 0 || order < 0) {
+    set_last_error("intbasis needs m >= 1, n >= 0, order >= 0");
+    return kInvalidArgument;
+  }
+  if (elem_bytes != 4) {
+    set_last_error("interpolant bases take uint32 operands (31-bit primes)");
+    return kUnsupported;
+  }
+  return intbasis_run(*ctx->cx, p, E, m, n, order, alpha, shift, ctx->pmbasis_T, P, order + 1,
+                      lp, rdeg_out);
+}
+
+int fpm_m_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E, int m, int n,
+                   int order, const uint64_t* alpha, const int64_t* shift, void* P, int* lp,
+                   int64_t* rdeg_out) {
+  // the iterative basis is the same product of canonical steps
+  return fpm_pm_intbasis(ctx, p, elem_bytes, E, m, n, order, alpha, shift, P, lp, rdeg_out);
+}
+
+int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const void* P, int m,
+                           int n, int L, const uint64_t* pts, int npts, void* out) {
+  if (!ctx || m < 0 || n < 0 || L < 0 || npts < 0 || (npts > 0 && !pts)) return kInvalidArgument;
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (elem_bytes != 4) {
+    set_last_error("point evaluation takes uint32 operands (31-bit primes)");
+    return kUnsupported;
+  }
+  return eval_points_run(*ctx->cx, p, P, m, n, L, pts, npts, out);
+}
+
 int fpm_profile_enable(fpm_context* ctx, int on) {
   if (!ctx) return kInvalidArgument;
   ctx->cx->profile_enable(on != 0);

@@ -29,6 +29,7 @@ enum Status : int {
   kLengthMismatch = 7,
   kOutOfRange = 8,
   kCompositeModulus = 9,
+  kDuplicatePoints = 10,
   kInvalidArgument = 20,
   kUnsupported = 21,
   kCudaError = 30,

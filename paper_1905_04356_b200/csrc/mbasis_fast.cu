@@ -228,6 +228,8 @@ __device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct, 
 struct StepArgs {
   const uint32_t* F;
   long long fs;
+  long long ts;           // F[e * fs + t * ts]: coefficient (or point) t of entry e
+  const uint32_t* alpha;  // interpolant points (m_intbasis), nullptr for approximants
   int lf, m, n, T;
   const int64_t* s;   // device shift (m)
   int* rec_np;        // [T] number of pivots
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
 
   for (int e = tid; e < (int)mn; e += kStepThreads) {
     const uint32_t* fe = a.F + (long long)e * a.fs;
-    for (int t = 0; t < T; ++t) G[(size_t)t * mn + e] = t < a.lf ? fe[t] : 0u;
+    for (int t = 0; t < T; ++t) G[(size_t)t * mn + e] = t < a.lf ? fe[(long long)t * a.ts] : 0u;
   }
   for (int i = tid; i < m; i += kStepThreads) sft[i] = a.s[i];
   __syncthreads();
@@ -619,11 +621,24 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     }
     __syncthreads();
     STEP_TRACE(3);
-    // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k) ----
-    for (int idx = tid; idx < np * n; idx += kStepThreads) {
-      const int i = plist[idx / n], j = idx - (idx / n) * n;
-      for (int t = T - 1; t >= k + 1; --t)
-        G[(size_t)t * mn + (size_t)i * n + j] = G[(size_t)(t - 1) * mn + (size_t)i * n + j];
+    if (a.alpha) {
+      // ---- interpolants: pivot rows times (x - alpha_k), so their residual
+      // at point t (> k) is scaled by alpha_t - alpha_k (appint.py:79-117) ----
+      const uint32_t ak = a.alpha[k];
+      for (int idx = tid; idx < np * n * (T - k - 1); idx += kStepThreads) {
+        const int t = k + 1 + idx / (np * n), r = idx - (idx / (np * n)) * (np * n);
+        const int i = plist[r / n], j = r - (r / n) * n;
+        const uint32_t d = a.alpha[t] >= ak ? a.alpha[t] - ak : a.alpha[t] + p - ak;
+        uint32_t* g = G + (size_t)t * mn + (size_t)i * n + j;
+        *g = mulmod(*g, d, f);
+      }
+    } else {
+      // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k) ----
+      for (int idx = tid; idx < np * n; idx += kStepThreads) {
+        const int i = plist[idx / n], j = idx - (idx / n) * n;
+        for (int t = T - 1; t >= k + 1; --t)
+          G[(size_t)t * mn + (size_t)i * n + j] = G[(size_t)(t - 1) * mn + (size_t)i * n + j];
+      }
     }
     for (int i = tid; i < m; i += kStepThreads) sft[i] += piv[i];
     __syncthreads();
@@ -641,6 +656,7 @@ struct BuildArgs {
   long long ps;
   int fold_k;
   F31 f;
+  const uint32_t* alpha;  // interpolants: pivot rows times (x - alpha_k)
 };
 
 // one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j.  Every step's
@@ -715,8 +731,14 @@ __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
     for (int idx = tid; idx < (L + 1) * np; idx += NT) {
       const int t = idx / np, q = idx - (idx / np) * np;
       const int i = pl[q];
-      if (t < L) Pp[t * m + q] = P0[(size_t)t * m + i];
-      P1[(size_t)t * m + i] = t >= 1 ? P0[(size_t)(t - 1) * m + i] : 0u;
+      const uint32_t cur = t < L ? P0[(size_t)t * m + i] : 0u;
+      if (t < L) Pp[t * m + q] = cur;
+      uint32_t v = t >= 1 ? P0[(size_t)(t - 1) * m + i] : 0u;
+      if (a.alpha) {  // x P - alpha_k P
+        const uint32_t ac = mulmod(cur, a.alpha[k], a.f);
+        v = v >= ac ? v - ac : v + a.f.p - ac;
+      }
+      P1[(size_t)t * m + i] = v;
     }
     __syncthreads();
     for (int idx = tid; idx < (L + 1) * nk; idx += NT) {
@@ -797,7 +819,8 @@ int mbasis_fast_max_order(int m, int n) {
 }
 
 int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long fs, int lf,
-                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev) {
+                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev,
+                const uint32_t* alpha_dev, long long ts) {
   if (order < 1 || order > mbasis_fast_max_order(m, n)) {
     set_last_error("mbasis_fast: shape m=%d n=%d order=%d exceeds shared memory", m, n, order);
     return kUnsupported;
@@ -814,6 +837,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   const int K = fold_period(p);
   StepArgs sa{};
   sa.F = (const uint32_t*)F; sa.fs = fs; sa.lf = lf < order ? lf : order;
+  sa.ts = ts; sa.alpha = alpha_dev;
   sa.m = m; sa.n = n; sa.T = order; sa.s = s_dev;
   sa.rec_np = rec_np; sa.rec_plist = rec_plist; sa.rec_Ct = rec_Ct;
   sa.sft_out = sft_dev; sa.fold_k = K; sa.f = f;
@@ -834,6 +858,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   }
   BuildArgs ba{};
   ba.rec_np = rec_np; ba.rec_plist = rec_plist; ba.rec_Ct = rec_Ct; ba.m = m; ba.T = order;
+  ba.alpha = alpha_dev;
   ba.P = (uint32_t*)P; ba.ps = ps; ba.fold_k = K; ba.f = f;
   const size_t bsmem = build_smem(m, order);
   static size_t battr = 0;

@@ -22,7 +22,8 @@
 namespace fpm {
 int mbasis_fast_max_order(int m, int n);
 int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long fs, int lf,
-                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev);
+                int order, const int64_t* s_dev, void* P, long long ps, int64_t* sft_dev,
+                const uint32_t* alpha_dev = nullptr, long long ts = 1);
 }  // namespace fpm
 
 namespace fpm {

@@ -16,4 +16,11 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
                 int lf, int order, const int64_t* shift, int T, void* P, long long ps, int* lp,
                 int64_t* rdeg_out);
 
+// interpolant bases (intbasis.cu): E point-major [order][m][n], host points
+int intbasis_run(Context& cx, uint64_t p, const void* E, int m, int n, int order,
+                 const uint64_t* alpha_host, const int64_t* shift, int T, void* P, long long ps,
+                 int* lp, int64_t* rdeg_out);
+int eval_points_run(Context& cx, uint64_t p, const void* P, int m, int n, int L,
+                    const uint64_t* pts_host, int npts, void* out);
+
 }  // namespace fpm

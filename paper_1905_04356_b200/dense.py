@@ -142,6 +142,48 @@ def mbasis_dense(F, order, s, p):
     return _basis("fpm_mbasis", F, order, s, p)
 
 
+def intbasis_dense(E, alpha, s, p):
+    """appint.pm_intbasis / m_intbasis (appint.py:208-319) on device data:
+    E (order, m, n) point-major constant matrices, alpha (order,) host points.
+    -> (P (m, m, deg+1), rdeg_s(P))."""
+    import torch
+
+    _check_tensor(E, p, "E")
+    order, m, n = E.shape
+    if len(alpha) != order:
+        from .errors import LengthMismatch
+
+        raise LengthMismatch("one point per constant matrix")
+    s_arr = (ctypes.c_int64 * max(m, 1))(*[int(x) for x in s])
+    a_arr = (ctypes.c_uint64 * max(order, 1))(*[int(x) % p for x in alpha])
+    P = torch.zeros((m, m, order + 1), dtype=E.dtype, device=E.device)
+    lp = ctypes.c_int(0)
+    rd = (ctypes.c_int64 * max(m, 1))()
+    h = _lib.context(E.device.index)
+    _lib.check(_lib.lib().fpm_pm_intbasis(h, p, elem_bytes_for(p), E.data_ptr(), m, n, order,
+                                          a_arr, s_arr, P.data_ptr(), ctypes.byref(lp), rd),
+               "fpm_pm_intbasis")
+    return P[:, :, : lp.value], [int(rd[i]) for i in range(m)]
+
+
+def eval_points_dense(P, pts, p):
+    """appint.eval_polmat_points (appint.py:262-287): P (m, n, L) device ->
+    (npts, m, n) values P(x) for x in pts."""
+    import torch
+
+    _check_tensor(P, p, "P")
+    m, n, L = P.shape
+    out = torch.empty((len(pts), m, n), dtype=P.dtype, device=P.device)
+    if not pts:
+        return out
+    a_arr = (ctypes.c_uint64 * len(pts))(*[int(x) % p for x in pts])
+    h = _lib.context(P.device.index)
+    _lib.check(_lib.lib().fpm_polmat_eval_points(h, p, elem_bytes_for(p), P.data_ptr(), m, n, L,
+                                                 a_arr, len(pts), out.data_ptr()),
+               "fpm_polmat_eval_points")
+    return out
+
+
 def ntt_dense(x, p, log_len, inverse=False):
     """Batched modring.ntt_forward / ntt_inverse on a (batch, 2^log_len) tensor."""
     import torch
