@@ -33,6 +33,8 @@ CONFIGS = {
     "cfg3": dict(kind="mul", p=P60, m=16, k=16, n=16, deg=2047),
     "cfg4": dict(kind="pmbasis", p=P31, m=64, n=32, sigma=4096),
     "cfg5": dict(kind="mul", p=P31, m=256, k=256, n=256, deg=2047),
+    # not a BASELINE config: the interpolant-basis row of SURVEY 8(f), cfg4's shape
+    "ib4": dict(kind="intbasis", p=P31, m=64, n=32, sigma=4096),
 }
 CRT_PRIMES = [2130706433, 2113929217, 2013265921, 1811939329, 1711276033, 1224736769,
               1107296257]
@@ -325,6 +327,17 @@ def make_inputs(cfg, device, seed):
     if cfg["kind"] == "mul":
         L = cfg["deg"] + 1
         return rnd((cfg["m"], cfg["k"], L)), rnd((cfg["k"], cfg["n"], L))
+    if cfg["kind"] == "intbasis":
+        # sigma constant m x n matrices at a geometric progression of points
+        import random as _r
+
+        rr = _r.Random(seed)
+        a0, ratio = rr.randrange(1, p), rr.randrange(2, p)
+        pts, cur = [], a0
+        for _ in range(cfg["sigma"]):
+            pts.append(cur)
+            cur = cur * ratio % p
+        return rnd((cfg["sigma"], cfg["m"], cfg["n"])), pts
     return (rnd((cfg["m"], cfg["n"], cfg["sigma"])),)
 
 
@@ -333,6 +346,8 @@ def run_step(cfg, inputs, out=None):
 
     if cfg["kind"] == "mul":
         return dense.pm_mul_dense(inputs[0], inputs[1], cfg["p"], out=out)
+    if cfg["kind"] == "intbasis":
+        return dense.intbasis_dense(inputs[0], inputs[1], [0] * cfg["m"], cfg["p"])[0]
     return dense.pmbasis_dense(inputs[0], cfg["sigma"], [0] * cfg["m"], cfg["p"])[0]
 
 
@@ -488,10 +503,14 @@ def per_config_table(device):
     for name, cfg in CONFIGS.items():
         try:
             inputs = make_inputs(cfg, device, 100 + int(name[-1]))
-            steps, warm = (3, 1) if cfg["kind"] == "pmbasis" else (10, 3)
+            steps, warm = (3, 1) if cfg["kind"] in ("pmbasis", "intbasis") else (10, 3)
             ts, _, _ = time_steps(cfg, inputs, steps, warm, flush)
             ts.sort()
             ms = ts[len(ts) // 2]
+            if cfg["kind"] == "intbasis":
+                out[name] = {"ms": round(ms, 4), "note": "PM-IntBasis (SURVEY 8(f) rank 2), "
+                             "not a BASELINE config"}
+                continue
             work = mul_work(cfg)[0] if cfg["kind"] == "mul" else pmbasis_work(cfg)
             out[name] = {"ms": round(ms, 4), "Gmodmul_s": round(work / ms / 1e6, 2)}
             del inputs
