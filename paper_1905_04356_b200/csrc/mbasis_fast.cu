@@ -103,8 +103,9 @@ __device__ __forceinline__ uint32_t redc3(uint32_t d, uint32_t v, uint32_t al, u
 // exactly the rows in rank order as pivots and the kernel coefficients are the
 // unique C = R_K R_P^-1; the left block ends diagonal (d_q) and the right
 // block is D C^T, so Ct[q][kr] = -right[q][kr] / d_q with no product phase.
-// Thread (gi, gs) holds row gi, columns gs + 16u.  Returns false (uniformly)
-// on a zero leading minor; W and the shared step state are then untouched.
+// Thread (gi, gs) holds row gi, columns gs + 16u.  W is R_k with row stride
+// NC + 1 (conflict-free column reads).  Returns false (uniformly) on a zero
+// leading minor; the shared step state is then untouched.
 template <int NC>
 __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int* klist,
                             uint32_t* pbuf, const F31& f, uint32_t* Ct, uint32_t* recC,
@@ -115,7 +116,8 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int col = gs + 16 * u;
-    v[u] = col < NC ? W[ord[col] * NC + gi] : (col < m ? W[klist[col - NC] * NC + gi] : 0u);
+    v[u] = col < NC ? W[ord[col] * (NC + 1) + gi]
+                    : (col < m ? W[klist[col - NC] * (NC + 1) + gi] : 0u);
   }
 #pragma unroll
   for (int c = 0; c < NC; c += 2) {
@@ -280,8 +282,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
 
   for (int k = 0; k < T; ++k) {
     const uint32_t* Gk = G + (size_t)k * mn;
-    for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
     const bool pairs_shape = n == 32 && m > n && m <= 64;  // solve_pairs
+    if (pairs_shape) {
+      // the pair solve reads R_k column-wise: a copy with row stride n + 1
+      // (in X, unused on that path) makes those reads bank-conflict free
+      for (int idx = tid; idx < (int)mn; idx += kStepThreads)
+        X[(idx / n) * (n + 1) + (idx - (idx / n) * n)] = Gk[idx];
+    } else {
+      for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
+    }
     const bool try_fast = !pairs_shape && m > n && n <= 32 && 2 * n * n + n * (m - n + 1) <= m * m;
     if (!try_fast && !pairs_shape)
       for (int idx = tid; idx < m * m; idx += kStepThreads)
@@ -333,11 +342,13 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
         if (tid == 0) s_nk = base;
       }
       __syncthreads();
-      if (solve_pairs<32>(W, m, ord, klist, sbuf, f, W, a.rec_Ct + (size_t)k * m * m,
+      if (solve_pairs<32>(X, m, ord, klist, sbuf, f, W, a.rec_Ct + (size_t)k * m * m,
                           a.trace ? a.trace + k * 8 : nullptr)) {
         fast_done = pairs_done = true;
       } else {
-        // degenerate residual: the general elimination starts from X = I
+        // degenerate residual: the general elimination on W = R_k from X = I
+        __syncthreads();
+        for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
         for (int i = tid; i < m; i += kStepThreads) piv[i] = 0;
         for (int idx = tid; idx < m * m; idx += kStepThreads)
           X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
