@@ -228,14 +228,21 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
   pdl_trigger();
 
   const long long items = a.n1 + a.n2;
-  const long long step = (long long)gridDim.x * G;
-  long long item = (long long)blockIdx.x * G + g;
+  // point quads: groups take items round-robin across the whole grid, so
+  // the eight entries sharing a 128-byte quad line are stored close in time;
+  // blocked rows own their lines: a contiguous range per CTA (every SM gets
+  // floor or ceil of items / CTAs)
+  const long long total = items;
+  const bool rr = PL == 2;
+  const long long hi = rr ? total : total * (blockIdx.x + 1) / gridDim.x;
+  const long long step = rr ? (long long)gridDim.x * G : G;
+  long long item = rr ? (long long)blockIdx.x * G + g : total * blockIdx.x / gridDim.x + g;
   const uint32_t bytes = (uint32_t)a.len * 4u;
   auto src_of = [&](long long it) -> const uint32_t* {
     return it < a.n1 ? a.in1 + z * a.in1_ps + it * a.in1_stride
                      : a.in2 + z * a.in2_ps + (it - a.n1) * a.in2_stride;
   };
-  if (leader && item < items) {
+  if (leader && item < hi) {
     expect_tx(mbar, bytes);
     bulk_load(inb_s, src_of(item), bytes, mbar);
   }
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
   const uint8_t* top_row = tab + lt * kRowBytes;
   const uint8_t* mid_row = tab + (T::TOP_ROWS + (lt & (T::MID_ROWS - 1))) * kRowBytes;
   uint32_t phase = 0;
-  for (; item < items; item += step) {
+  for (; item < hi; item += step) {
     tc::mbar_wait_a(mbar, phase);
     phase ^= 1u;
     uint32_t v[32];
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
     row_apply_t<true>(v, top_row, p);
     if (leader) bulk_wait_read0();  // the previous output store has read the tile
     gsync(bar, T::TPT);             // input reads done, tile free
-    if (leader && item + step < items) {
+    if (leader && item + step < hi) {
       expect_tx(mbar, bytes);
       bulk_load(inb_s, src_of(item + step), bytes, mbar);
     }
@@ -334,8 +341,12 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
   pdl_wait();
   pdl_trigger();
 
-  const long long step = (long long)gridDim.x * G;
-  long long item = (long long)blockIdx.x * G + g;
+  // contiguous item range per CTA (its groups interleave inside it): every
+  // SM gets floor or ceil of items / CTAs, not whole rounds of G
+  const long long total = a.n;
+  const long long hi = total * (blockIdx.x + 1) / gridDim.x;
+  const long long step = G;
+  long long item = total * blockIdx.x / gridDim.x + g;
   auto load = [&](long long it) {
     expect_tx(mbar, (uint32_t)T::N * 4u);
     if constexpr (PL == 5) {
@@ -345,11 +356,11 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
       for (int c = 0; c < 8; ++c) tma_load_5d(inb_s + c * (T::N / 2), &im, mbar, 0, (int)it, c, 0, z);
     }
   };
-  if (leader && item < a.n) load(item);
+  if (leader && item < hi) load(item);
   const uint8_t* top_row = tab + lt * kRowBytes;
   const uint8_t* mid_row = tab + (T::TOP_ROWS + (lt & (T::MID_ROWS - 1))) * kRowBytes;
   uint32_t phase = 0;
-  for (; item < a.n; item += step) {
+  for (; item < hi; item += step) {
     tc::mbar_wait_a(mbar, phase);
     phase ^= 1u;
     uint32_t v[32];
@@ -363,7 +374,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
     // input buffer read by every thread (the next transform may land), and the
     // previous transform's last tile reads are done (tile free)
     gsync(bar, T::TPT);
-    if (leader && item + step < a.n) load(item + step);
+    if (leader && item + step < hi) load(item + step);
     to_smem<LOGN, MAP_LAST>(tile, v, lt);
     gsync(bar, T::TPT);
     from_smem<LOGN, MAP_MID>(tile, v, lt);
