@@ -192,7 +192,7 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   FPM_TRY(ws.get(esz * nb + 1, &dB));
   FPM_TRY(ws.get(esz * nc + 1, &dC));
   static const int force = std::getenv("FPM_HOST_BLOCKS") ? std::atoi(std::getenv("FPM_HOST_BLOCKS")) : 0;
-  int R = force > 0 ? force : (esz * nc >= (256u << 20) ? 4 : esz * nc >= (8u << 20) ? 2 : 1);
+  int R = force > 0 ? force : (esz * nc >= (256u << 20) ? 4 : esz * nc >= (8u << 20) ? 3 : 1);
   if (R > m) R = m;
   if (R > n) R = n;
   if (R <= 1 || lc == 0) {
@@ -232,9 +232,18 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   // each row block of A and column block of B is transformed once and its
   // evaluations reused by the other blocks of its row / column
   std::vector<EvalCache> ca(R), cb(R);
-  for (int i = 0; i < R && status == kOk; ++i) {
+  // blocks in shells of max(i, j): shell s adds A_s and B_s and 2s + 1
+  // computable blocks, so the copy-out stream starts after one block's
+  // inputs and is fed faster than row-major order feeds it
+  std::vector<std::pair<int, int>> order;
+  for (int sh = 0; sh < R; ++sh) {
+    for (int j = 0; j <= sh; ++j) order.push_back({sh, j});
+    for (int i = 0; i < sh; ++i) order.push_back({i, sh});
+  }
+  for (size_t ob = 0; ob < order.size() && status == kOk; ++ob) {
+    const int i = order[ob].first, j = order[ob].second;
     const int i0 = lo(i, m), i1 = lo(i + 1, m), ib = i1 - i0;
-    for (int j = 0; j < R && status == kOk; ++j) {
+    {
       const int j0 = lo(j, n), j1 = lo(j + 1, n), jb = j1 - j0;
       unsigned char* dAi = dA + esz * (size_t)i0 * k * la;
       unsigned char* dBj = dB + esz * (size_t)k * j0 * lb;  // column block j, packed [k][jb][lb]
