@@ -176,9 +176,10 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
 // kernel rows kr of one R-row block and 4 columns j.  Smaller R spreads a
 // short list (few t) over all threads instead of leaving most of them idle.
 template <int R>
-__device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct, const int* klist,
-                                               const int* plist, int n, int nk, int np, int k,
-                                               int nt, size_t mn, const F31& f) {
+__device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct,
+                                               const long long* krow, const long long* prow,
+                                               int n, int nk, int np, int k, int nt, size_t mn,
+                                               const F31& f) {
   const int rb_n = nk / R, cb_n = n >> 2;
   const int blocks = rb_n * cb_n * nt;
   for (int b = threadIdx.x; b < blocks; b += blockDim.x) {
@@ -186,17 +187,17 @@ __device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct, 
     const int rem = b - (b / (rb_n * cb_n)) * (rb_n * cb_n);
     const int rb = rem / cb_n, cb = rem - (rem / cb_n) * cb_n;
     uint32_t* Gt = G + (size_t)t * mn;
-    int rows[R];
+    long long rows[R];
     uint64_t acc[R][4];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      rows[r] = klist[rb * R + r];
-      const uint4 g = *reinterpret_cast<const uint4*>(Gt + (size_t)rows[r] * n + cb * 4);
+      rows[r] = krow[rb * R + r];
+      const uint4 g = *reinterpret_cast<const uint4*>(Gt + rows[r] + cb * 4);
       acc[r][0] = g.x; acc[r][1] = g.y; acc[r][2] = g.z; acc[r][3] = g.w;
     }
 #pragma unroll 4
     for (int q = 0; q < np; ++q) {
-      const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + (size_t)plist[q] * n + cb * 4);
+      const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + prow[q] + cb * 4);
       const uint32_t gv[4] = {g4.x, g4.y, g4.z, g4.w};
       uint32_t cv[R];
       if constexpr (R == 4) {
@@ -221,7 +222,7 @@ __device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct, 
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      *reinterpret_cast<uint4*>(Gt + (size_t)rows[r] * n + cb * 4) =
+      *reinterpret_cast<uint4*>(Gt + rows[r] + cb * 4) =
           make_uint4(d_red64(acc[r][0], f.p, f.mu), d_red64(acc[r][1], f.p, f.mu),
                      d_red64(acc[r][2], f.p, f.mu), d_red64(acc[r][3], f.p, f.mu));
   }
@@ -266,6 +267,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   int* piv = ord + m;                             // m
   int* plist = piv + m;                           // m
   int* klist = plist + m;                         // m
+  // Per-row coefficient offsets: multiplying pivot row i by x shifts its
+  // residual coefficients (G[t][i] <- G[t-1][i]); instead of moving data the
+  // row's offset grows, coefficient t of row i living in slot t - off[i].
+  // rowoff[i] = i*n - off[i]*mn, so G[t][i] starts at G + t*mn + rowoff[i].
+  int* off = klist + m;                           // m
+  long long* rowoff = (long long*)(((uintptr_t)(off + m) + 7) & ~(uintptr_t)7);  // m
+  long long* prow = rowoff + m;                   // m: rowoff[plist[q]] of the step
+  long long* krow = prow + m;                     // m: rowoff[klist[kr]] of the step
   __shared__ int s_key[2];
   __shared__ int s_nk;
   __shared__ uint32_t sbuf[2 * 128];  // block solves: pivot rows (+ column), double buffered
@@ -277,19 +286,27 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     const uint32_t* fe = a.F + (long long)e * a.fs;
     for (int t = 0; t < T; ++t) G[(size_t)t * mn + e] = t < a.lf ? fe[(long long)t * a.ts] : 0u;
   }
-  for (int i = tid; i < m; i += kStepThreads) sft[i] = a.s[i];
+  for (int i = tid; i < m; i += kStepThreads) {
+    sft[i] = a.s[i];
+    off[i] = 0;
+    rowoff[i] = (long long)i * n;
+  }
   __syncthreads();
 
   for (int k = 0; k < T; ++k) {
-    const uint32_t* Gk = G + (size_t)k * mn;
+    const uint32_t* Gk = G + (size_t)k * mn;  // + rowoff[i] - i*n per row
+    auto gk = [&](int idx) {
+      const int i = idx / n;
+      return Gk[rowoff[i] + (idx - i * n)];
+    };
     const bool pairs_shape = n == 32 && m > n && m <= 64;  // solve_pairs
     if (pairs_shape) {
       // the pair solve reads R_k column-wise: a copy with row stride n + 1
       // (in X, unused on that path) makes those reads bank-conflict free
       for (int idx = tid; idx < (int)mn; idx += kStepThreads)
-        X[(idx / n) * (n + 1) + (idx - (idx / n) * n)] = Gk[idx];
+        X[(idx / n) * (n + 1) + (idx - (idx / n) * n)] = gk(idx);
     } else {
-      for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
+      for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = gk(idx);
     }
     const bool try_fast = !pairs_shape && m > n && n <= 32 && 2 * n * n + n * (m - n + 1) <= m * m;
     if (!try_fast && !pairs_shape)
@@ -348,7 +365,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
       } else {
         // degenerate residual: the general elimination on W = R_k from X = I
         __syncthreads();
-        for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = Gk[idx];
+        for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = gk(idx);
         for (int i = tid; i < m; i += kStepThreads) piv[i] = 0;
         for (int idx = tid; idx < m * m; idx += kStepThreads)
           X[idx] = (idx / m == idx - (idx / m) * m) ? 1u : 0u;
@@ -550,14 +567,17 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     STEP_TRACE(2);
 
     // ---- residual list: kernel rows G[t][i] += sum_q Ct G[t][plist[q]], t > k -
+    for (int q = tid; q < np; q += kStepThreads) prow[q] = rowoff[plist[q]];
+    for (int kr = tid; kr < nk; kr += kStepThreads) krow[kr] = rowoff[klist[kr]];
+    __syncthreads();
     if (((n | nk) & 3) == 0 && a.fold_k == 4) {
       const int nt = T - k - 1;
       if (nt <= 2)
-        residual_tiles<1>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+        residual_tiles<1>(G, Ct, krow, prow, n, nk, np, k, nt, mn, f);
       else if (nt <= 4)
-        residual_tiles<2>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+        residual_tiles<2>(G, Ct, krow, prow, n, nk, np, k, nt, mn, f);
       else
-        residual_tiles<4>(G, Ct, klist, plist, n, nk, np, k, nt, mn, f);
+        residual_tiles<4>(G, Ct, krow, prow, n, nk, np, k, nt, mn, f);
     } else {
       const int rb_n = (nk + 3) >> 2, cb_n = (n + 3) >> 2, nt = T - k - 1;
       const int blocks = rb_n * cb_n * nt;
@@ -576,14 +596,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             const int j = cb * 4 + cc;
-            acc[r][cc] = (rows[r] >= 0 && j < n) ? Gt[(size_t)rows[r] * n + j] : 0;
+            acc[r][cc] = (rows[r] >= 0 && j < n) ? Gt[krow[rb * 4 + r] + j] : 0;
           }
         }
         if (((n | nk) & 3) == 0 && K == 4) {
           // aligned fast path: 16-byte shared loads, folds at fixed positions
 #pragma unroll 4
           for (int q = 0; q < np; ++q) {
-            const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + (size_t)plist[q] * n + cb * 4);
+            const uint4 g4 = *reinterpret_cast<const uint4*>(Gt + prow[q] + cb * 4);
             const uint4 c4 = *reinterpret_cast<const uint4*>(Ct + q * nk + rb * 4);
             const uint32_t gv[4] = {g4.x, g4.y, g4.z, g4.w}, cv[4] = {c4.x, c4.y, c4.z, c4.w};
 #pragma unroll
@@ -600,7 +620,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
         } else {
           int cnt = 0;
           for (int q = 0; q < np; ++q) {
-            const uint32_t* gl = Gt + (size_t)plist[q] * n + cb * 4;
+            const uint32_t* gl = Gt + prow[q] + cb * 4;
             uint32_t gv[4], cv[4];
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) gv[cc] = (cb * 4 + cc < n) ? gl[cc] : 0u;
@@ -625,7 +645,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             const int j = cb * 4 + cc;
-            if (j < n) Gt[(size_t)rows[r] * n + j] = d_red64(acc[r][cc], p, f.mu);
+            if (j < n) Gt[krow[rb * 4 + r] + j] = d_red64(acc[r][cc], p, f.mu);
           }
         }
       }
@@ -640,15 +660,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
         const int t = k + 1 + idx / (np * n), r = idx - (idx / (np * n)) * (np * n);
         const int i = plist[r / n], j = r - (r / n) * n;
         const uint32_t d = a.alpha[t] >= ak ? a.alpha[t] - ak : a.alpha[t] + p - ak;
-        uint32_t* g = G + (size_t)t * mn + (size_t)i * n + j;
+        uint32_t* g = G + (size_t)t * mn + rowoff[i] + j;
         *g = mulmod(*g, d, f);
       }
     } else {
-      // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k) ----
-      for (int idx = tid; idx < np * n; idx += kStepThreads) {
-        const int i = plist[idx / n], j = idx - (idx / n) * n;
-        for (int t = T - 1; t >= k + 1; --t)
-          G[(size_t)t * mn + (size_t)i * n + j] = G[(size_t)(t - 1) * mn + (size_t)i * n + j];
+      // ---- pivot rows: G_i <- x G_i (coefficient t takes t-1; k+1 takes R_k):
+      // the row's offset grows, no data moves ----
+      for (int q = tid; q < np; q += kStepThreads) {
+        const int i = plist[q];
+        off[i] += 1;
+        rowoff[i] -= (long long)mn;
       }
     }
     for (int i = tid; i < m; i += kStepThreads) sft[i] += piv[i];
@@ -806,7 +827,7 @@ F31 make_f31(uint32_t p) {
 
 size_t steps_smem(int m, int n, int T) {
   return 8 * (size_t)m + 4 * ((size_t)T * m * n + (size_t)m * n + (size_t)m * m + m) +
-         4 * 5 * (size_t)m;
+         4 * 6 * (size_t)m + 8 + 8 * 3 * (size_t)m;
 }
 
 }  // namespace
