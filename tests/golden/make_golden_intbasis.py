@@ -51,6 +51,11 @@ def main():
         (7, 2013265921, 8, 2, 64, [-3, 0, 7, 1, 1, 0, 2, 9], False, 5, "pm"),
         (8, 2013265921, 16, 8, 256, [0] * 16, True, 0, "pm"),
         (9, 2013265921, 12, 5, 150, [0] * 12, False, 0, "pm"),
+        (10, 2013265921, 2, 3, 12, [0, 0], False, 0, "pm"),          # m < n
+        (14, 2013265921, 4, 4, 30, [1, 0, 0, 2], False, 4, "pm"),    # m = n
+        (15, 3, 3, 2, 3, [0, 0, 0], False, 0, "m"),                  # p = 3, all points
+        (16, 2013265921, 40, 32, 64, [0] * 40, False, 7, "pm"),      # the n = 32 block solve
+        (17, 2013265921, 64, 32, 100, [0] * 64, True, 0, "pm"),      # cfg4 / ib4 shape
     ]
     for seed, p, m, n, order, shift, geo, ze, flavor in specs:
         ctx = field_new(p)

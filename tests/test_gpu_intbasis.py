@@ -39,7 +39,7 @@ def draw_case(seed, p, m, n, order, geometric=False, zero_every=0):
     return E, alpha
 
 
-@pytest.mark.parametrize("idx", range(9))
+@pytest.mark.parametrize("idx", range(14))
 def test_intbasis_matches_reference(idx):
     g = _golden()["cases"][idx]
     ctx = F.field_new(g["p"])
