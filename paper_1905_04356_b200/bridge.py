@@ -19,7 +19,8 @@ def _wrap(ref_polmat_cls, fn):
 
 
 def install_into_reference(fpmat_pkg=None):
-    """Rebind fpmat's pm_mul / _pm_middle / pmbasis / mbasis to the B200 path.
+    """Rebind fpmat's pm_mul / _pm_middle / pmbasis / mbasis / pm_intbasis /
+    m_intbasis / eval_polmat_points to the B200 path.
 
     Returns a dict {module.name: original} that ``uninstall`` restores."""
     import importlib
@@ -37,6 +38,9 @@ def install_into_reference(fpmat_pkg=None):
         "pm_middle_product": _wrap(RefPolMat, polmat.pm_middle_product),
         "pmbasis": _wrap(RefPolMat, appint.pmbasis),
         "mbasis": _wrap(RefPolMat, appint.mbasis),
+        "pm_intbasis": _wrap(RefPolMat, appint.pm_intbasis),
+        "m_intbasis": _wrap(RefPolMat, appint.m_intbasis),
+        "eval_polmat_points": appint.eval_polmat_points,
     }
     # import every module first so none binds an already-replaced name
     mods = []

@@ -6,10 +6,14 @@ kernel_direct(F, s) follows ref:kernel.py:42-76 (flavor "approx"): with
 d = deg F and the shift normalised to minimum 0, the order d + delta basis
 (delta = n d + max(s0) + 1) contains the kernel rows as its rows of s0-degree
 below delta; they are returned sorted by pivot (ref:kernel.py:35-40).  The
-"interp" flavor needs PM-IntBasis, outside this repository's scope.
+"interp" flavor evaluates F on a geometric progression of that length
+(modring.order_at_least) and takes the GPU PM-IntBasis instead
+(ref:kernel.py:58-70).
 """
-from .appint import pmbasis
+from .appint import eval_polmat_points, pm_intbasis, pmbasis
+from .errors import NoGeometricGrid, NoSuchElement
 from .forms import NEG_INF, pivot_profile, rdeg
+from .modring import order_at_least
 
 
 class KernelBasis:
@@ -35,13 +39,26 @@ def _by_pivot(M, s):
 def kernel_direct(F, s, flavor="approx"):
     if any(si < 0 for si in s):
         raise ValueError("kernel_direct expects a nonnegative shift")
-    if flavor != "approx":
-        raise ValueError(f"unsupported flavor {flavor!r} (only 'approx' is provided here)")
+    ctx = F.ctx
     m, n = F.m, F.n
     d = max(F.degree, 0)
     s0 = [si - min(s) for si in s] if s else []
     delta = n * d + (max(s0) if s0 else 0) + 1
-    P = pmbasis(F, d + delta, s0)
+    order = d + delta
+    if flavor == "approx":
+        P = pmbasis(F, order, s0)
+    elif flavor == "interp":
+        try:
+            alpha = order_at_least(ctx, order)
+        except NoSuchElement:
+            raise NoGeometricGrid(f"field has no geometric progression of length {order}")
+        pts = [1] * order
+        for i in range(1, order):
+            pts[i] = pts[i - 1] * alpha % ctx.p
+        E = eval_polmat_points(F, pts, ctx)  # pm_eval at every point (polmat.py:539-543)
+        P = pm_intbasis(E, pts, s0, ctx)
+    else:
+        raise ValueError(f"unknown flavor {flavor!r}")
     degs = rdeg(P, s0)
     keep = [i for i in range(m) if degs[i] != NEG_INF and degs[i] < delta]
     return KernelBasis(_by_pivot(P.submatrix(keep, range(m)), s), list(s), "owp")

@@ -40,3 +40,24 @@ def test_kernel_direct_matches_reference(idx):
     assert kb.K.rows == rec["K"]
     if kb.K.m:
         assert F.pm_mul(kb.K, Fm).is_zero()
+
+
+@pytest.mark.parametrize("idx", range(len(CALLERS["fracrec_points"])))
+def test_fracrec_points_matches_reference(idx):
+    """fracrec_points (fraction.py:72-97): one GPU PM-IntBasis at 2D points."""
+    rec = CALLERS["fracrec_points"][idx]
+    ctx = F.field_new(rec["p"])
+    d = F.fraction.fracrec_points(ctx, rec["Hvals"], rec["pts"], rec["D"])
+    assert d.Q.rows == rec["Q"] and d.R.rows == rec["R"]
+
+
+@pytest.mark.parametrize("idx", range(len(CALLERS["kernel_interp"])))
+def test_kernel_direct_interp_matches_reference(idx):
+    """kernel_direct(flavor="interp") (kernel.py:58-70): evaluation on a
+    geometric progression + GPU PM-IntBasis."""
+    rec = CALLERS["kernel_interp"][idx]
+    Fm = _pm(rec["p"], rec["F"], rec["n"])
+    kb = F.kernel.kernel_direct(Fm, rec["s"], flavor="interp")
+    assert kb.K.rows == rec["K"]
+    if kb.K.m:
+        assert F.pm_mul(kb.K, Fm).is_zero()
