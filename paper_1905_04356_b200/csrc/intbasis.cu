@@ -22,6 +22,8 @@
 
 #include "ops.cuh"
 #include "pmbasis.cuh"
+#include "runtime.cuh"
+#include "tc_pointwise.cuh"
 
 namespace fpm {
 int mbasis_fast_max_order(int m, int n);
@@ -112,6 +114,18 @@ int eval_points(Context& cx, uint32_t p, const uint32_t* P, long long ps, int L,
 int point_product(Context& cx, uint32_t p, const uint32_t* A, const uint32_t* B, uint32_t* R,
                   int m, int k, int n, int npts) {
   if (npts <= 0 || m <= 0 || n <= 0) return kOk;
+  // larger residual products on the int8 tensor cores: the operands are
+  // already point-major, the layout tc_grouped_kernel reads (as ops.cu, m > 32)
+  if (m > 32 && tc_grouped_applicable(m, k, n, p)) {
+    PrimeSet ps;
+    ps.count = 1;
+    FPM_TRY(cx.prime_const(p, 5, &ps.pr[0]));
+    TcArgs ta{};
+    ta.A = A; ta.B = B; ta.C = R; ta.m = m; ta.k = k; ta.n = n; ta.npts = npts;
+    ta.a_ps = (long long)npts * m * k; ta.b_ps = (long long)npts * k * n;
+    ta.c_ps = (long long)npts * m * n;
+    return launch_tc_grouped(ta, ps, cx.stream());
+  }
   const size_t smem = sizeof(uint32_t) * ((size_t)m * k + (size_t)k * n);
   if (smem > 200 * 1024) {
     set_last_error("interpolant residual: %d x %d x %d per point exceeds shared memory", m, k, n);
