@@ -9,15 +9,18 @@
 //   * leaves: the shared-memory M-Basis kernels in interpolant mode
 //     (mbasis_fast.cu: the residual list holds P(alpha_t) E_t and pivot rows
 //     are rescaled by alpha_t - alpha_k instead of shifted);
-//   * internal nodes: P1 is evaluated at the tail points (Horner, each thread
-//     one entry at 8 points, `eval_points_kernel`), the residuals
-//     R_t = P1(alpha_t) E_t are per-point products (`point_product_kernel`),
-//     then P = P2 * P1 on the NTT product path;
+//   * internal nodes: P1 is evaluated at the tail points -- by a chirp
+//     middle product on the NTT path when the points form a geometric
+//     progression (as the reference does), else by Horner (each thread one
+//     entry at 8 points, `eval_points_kernel`) -- the residuals
+//     R_t = P1(alpha_t) E_t are per-point products (int8 tensor cores via
+//     tc_grouped_kernel, or `point_product_kernel`), then P = P2 * P1 on the
+//     NTT product path;
 //   * shifts stay on the device (s <- s + delta through the leaves), lengths
 //     use deg P <= order: no host synchronisation inside the recursion.
-// Points are arbitrary distinct field elements (the reference's geometric
-// chirp evaluation is an optimisation of the same values).
+// Points are arbitrary distinct field elements.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ops.cuh"
@@ -111,6 +114,113 @@ int eval_points(Context& cx, uint32_t p, const uint32_t* P, long long ps, int L,
   return kOk;
 }
 
+// ---- geometric points: chirp (Bluestein) evaluation on the NTT path -------
+// With alpha_t = a0 r^t and C(u) = u(u-1)/2, r^(i j) = r^C(i+j) r^-C(i) r^-C(j),
+// so f(a0 r^j) = r^-C(j) sum_i (c_i a0^i r^-C(i)) r^C(i+j): one middle
+// product of the scaled coefficients with the chirp r^C(u) per entry
+// (ref upoly._eval_geometric_raw, upoly.py:455-472, used by
+// appint.eval_polmat_points for geometric points, appint.py:268-282).
+struct GeoPts {
+  bool on;
+  uint32_t r, rinv;
+};
+
+__device__ __forceinline__ uint32_t powmod_dev(uint32_t a, uint64_t e, uint32_t p, uint64_t mu) {
+  uint32_t r = 1u;
+  while (e) {
+    if (e & 1) r = d_red64((uint64_t)r * a, p, mu);
+    a = d_red64((uint64_t)a * a, p, mu);
+    e >>= 1;
+  }
+  return r;
+}
+
+// w[j] = a0^j r^-C(j) (j < la), tri[u] = r^C(u) (u < la + npts - 1),
+// tinv[j] = r^-C(j) (j < npts); a0 read on the device (no host round trip)
+__global__ void chirp_tables_kernel(const uint32_t* __restrict__ a0p, uint32_t r, uint32_t rinv,
+                                    int la, int npts, uint32_t p, uint64_t mu,
+                                    uint32_t* __restrict__ w, uint32_t* __restrict__ tri,
+                                    uint32_t* __restrict__ tinv) {
+  pdl_wait();
+  const uint32_t a0 = *a0p;
+  const int total = la + npts - 1;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < total; u += gridDim.x * blockDim.x) {
+    const uint64_t cu = ((uint64_t)u * (uint64_t)(u > 0 ? u - 1 : 0) / 2) % (p - 1);
+    tri[u] = powmod_dev(r, cu, p, mu);
+    if (u < la || u < npts) {
+      const uint32_t ri = powmod_dev(rinv, cu, p, mu);
+      if (u < npts) tinv[u] = ri;
+      if (u < la) w[u] = d_red64((uint64_t)powmod_dev(a0, (uint64_t)u, p, mu) * ri, p, mu);
+    }
+  }
+}
+
+// U[e][j] = P[e*ps + la-1-j] w[la-1-j]: scaled and reversed (the correlation
+// sum_i U_i r^C(i+j) becomes the product coefficient la-1+j)
+__global__ void scale_rows_kernel(const uint32_t* __restrict__ P, long long ps, int la, long long E,
+                                  const uint32_t* __restrict__ w, uint32_t p, uint64_t mu,
+                                  uint32_t* __restrict__ U) {
+  pdl_wait();
+  const long long total = E * la;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i / la;
+    const int j = la - 1 - (int)(i - e * la);
+    U[i] = d_red64((uint64_t)P[e * ps + j] * w[j], p, mu);
+  }
+}
+
+// EV[t][e] = M[e][t] tinv[t]: 32 x 32 tiles through shared memory
+__global__ void transpose_scale_kernel(const uint32_t* __restrict__ M, long long E, int npts,
+                                       const uint32_t* __restrict__ tinv, uint32_t p, uint64_t mu,
+                                       uint32_t* __restrict__ EV) {
+  pdl_wait();
+  __shared__ uint32_t tile[32][33];
+  const long long e0 = (long long)blockIdx.x * 32;
+  const int t0 = blockIdx.y * 32;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const long long e = e0 + r;
+    const int t = t0 + threadIdx.x;
+    tile[r][threadIdx.x] = (e < E && t < npts) ? M[e * npts + t] : 0u;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int t = t0 + r;
+    const long long e = e0 + threadIdx.x;
+    if (t < npts && e < E) EV[(long long)t * E + e] = d_red64((uint64_t)tile[threadIdx.x][r] * tinv[t], p, mu);
+  }
+}
+
+int eval_points_geo(Context& cx, uint32_t p, const uint32_t* P, long long ps, int la, long long E,
+                    const uint32_t* a0_dev, int npts, const GeoPts& g, uint32_t* EV) {
+  const uint64_t mu = (uint64_t)((((u128)1) << 64) / p);
+  const int lt = la + npts - 1;
+  Workspace ws(cx);
+  uint32_t *w, *tri, *tinv, *U, *Mv;
+  FPM_TRY(ws.get((size_t)la, &w));
+  FPM_TRY(ws.get((size_t)lt, &tri));
+  FPM_TRY(ws.get((size_t)npts, &tinv));
+  FPM_TRY(ws.get((size_t)E * la, &U));
+  FPM_TRY(ws.get((size_t)E * npts, &Mv));
+  const cudaStream_t st = cx.stream();
+  FPM_CUDA_TRY(launch_pdl(chirp_tables_kernel, dim3((unsigned)((lt + 255) / 256)), dim3(256), 0, st,
+                          a0_dev, g.r, g.rinv, la, npts, p, mu, w, tri, tinv));
+  FPM_LAUNCH_CHECK();
+  const long long tot = E * la;
+  FPM_CUDA_TRY(launch_pdl(scale_rows_kernel, dim3((unsigned)std::min<long long>((tot + 255) / 256, 148 * 16)),
+                          dim3(256), 0, st, P, ps, la, E, w, p, mu, U));
+  FPM_LAUNCH_CHECK();
+  MatRef A{U, 0, la, la};
+  MatRef B{tri, 0, lt, lt};
+  OutRef C{Mv, 0, npts, npts};
+  FPM_TRY(polmat_middle(cx, p, (int)E, 1, 1, A, B, la - 1, lt - 1, la - 1, npts, 1, C));
+  dim3 grid((unsigned)((E + 31) / 32), (unsigned)((npts + 31) / 32));
+  FPM_CUDA_TRY(launch_pdl(transpose_scale_kernel, grid, dim3(32, 8), 0, st, Mv, E, npts, tinv, p,
+                          mu, EV));
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
 int point_product(Context& cx, uint32_t p, const uint32_t* A, const uint32_t* B, uint32_t* R,
                   int m, int k, int n, int npts) {
   if (npts <= 0 || m <= 0 || n <= 0) return kOk;
@@ -148,7 +258,7 @@ int point_product(Context& cx, uint32_t p, const uint32_t* A, const uint32_t* B,
 // E: [order][m][n] point-major, alpha: [order] device
 int intbasis_rec_dev(Context& cx, uint32_t p, const uint32_t* E, const uint32_t* alpha, int m,
                      int n, int order, const int64_t* s_dev, int T, uint32_t* P, long long ps,
-                     int64_t* sft_dev) {
+                     int64_t* sft_dev, const GeoPts& geo) {
   if (order <= T)
     return mbasis_fast(cx, p, E, m, n, 1, order, order, s_dev, P, ps, sft_dev, alpha,
                        (long long)m * n);
@@ -158,14 +268,19 @@ int intbasis_rec_dev(Context& cx, uint32_t p, const uint32_t* E, const uint32_t*
   int64_t* s1;
   FPM_TRY(ws.get((size_t)m * m * (o1 + 1), &P1));
   FPM_TRY(ws.get((size_t)m, &s1));
-  FPM_TRY(intbasis_rec_dev(cx, p, E, alpha, m, n, o1, s_dev, T, P1, o1 + 1, s1));
+  FPM_TRY(intbasis_rec_dev(cx, p, E, alpha, m, n, o1, s_dev, T, P1, o1 + 1, s1, geo));
   // residuals of the tail points: R_t = P1(alpha_t) E_t (appint.py:300-312)
   FPM_TRY(ws.get((size_t)o2 * m * m, &EV));
   FPM_TRY(ws.get((size_t)o2 * m * n, &R));
-  FPM_TRY(eval_points(cx, p, P1, o1 + 1, o1 + 1, (long long)m * m, alpha + o1, o2, EV));
+  // geometric tail points of a long P1: chirp evaluation (NTT path),
+  // otherwise Horner (the reference switches at degree 16, appint.py:268)
+  if (geo.on && o1 + 1 >= 64 && o2 >= 64)
+    FPM_TRY(eval_points_geo(cx, p, P1, o1 + 1, o1 + 1, (long long)m * m, alpha + o1, o2, geo, EV));
+  else
+    FPM_TRY(eval_points(cx, p, P1, o1 + 1, o1 + 1, (long long)m * m, alpha + o1, o2, EV));
   FPM_TRY(point_product(cx, p, EV, E + (size_t)o1 * m * n, R, m, m, n, o2));
   FPM_TRY(ws.get((size_t)m * m * (o2 + 1), &P2));
-  FPM_TRY(intbasis_rec_dev(cx, p, R, alpha + o1, m, n, o2, s1, T, P2, o2 + 1, sft_dev));
+  FPM_TRY(intbasis_rec_dev(cx, p, R, alpha + o1, m, n, o2, s1, T, P2, o2 + 1, sft_dev, geo));
   MatRef A2{P2, 0, o2 + 1, o2 + 1};
   MatRef B2{P1, 0, o1 + 1, o1 + 1};
   OutRef Co{P, 0, ps, (int)ps};
@@ -192,6 +307,20 @@ int intbasis_run(Context& cx, uint64_t p, const void* E, int m, int n, int order
       set_last_error("interpolation points must be pairwise distinct");
       return kDuplicatePoints;
     }
+  }
+  // geometric progression (appint._is_geometric, appint.py:248-259): every
+  // contiguous range of the points is then one as well, with the same ratio
+  GeoPts geo{false, 1u, 1u};
+  if (order >= 3 && pts[0] != 0 && pts[1] != 0) {
+    const uint64_t r = h_mulmod(pts[1], h_invmod(pts[0], p), p);
+    bool ok = true;
+    uint64_t cur = pts[1];
+    for (int t = 2; t < order && ok; ++t) {
+      cur = h_mulmod(cur, r, p);
+      ok = cur == pts[t];
+    }
+    static const bool off = std::getenv("FPM_NO_CHIRP") != nullptr;
+    if (ok && !off) geo = GeoPts{true, (uint32_t)r, (uint32_t)h_invmod(r, p)};
   }
   if (T < 1) T = 1;
   const int tf = mbasis_fast_max_order(m, n);
@@ -225,7 +354,7 @@ int intbasis_run(Context& cx, uint64_t p, const void* E, int m, int n, int order
     return kOk;
   }
   FPM_TRY(intbasis_rec_dev(cx, (uint32_t)p, (const uint32_t*)E, a_dev, m, n, order, s_dev, T,
-                           (uint32_t*)P, ps, sft_dev));
+                           (uint32_t*)P, ps, sft_dev, geo));
   int deg = -1;
   FPM_TRY(matrix_degree(cx, P, 0, (long long)m * m, (int)ps, &deg));  // synchronizes
   *lp = deg + 1;
@@ -249,6 +378,21 @@ int eval_points_run(Context& cx, uint64_t p, const void* P, int m, int n, int L,
   FPM_TRY(ws.get((size_t)npts, &a_dev));
   FPM_CUDA_TRY(cudaMemcpyAsync(a_dev, pts.data(), sizeof(uint32_t) * npts,
                                cudaMemcpyHostToDevice, cx.stream()));
+  // geometric points and degree >= 16: the chirp route (appint.py:268-282)
+  if (npts >= 3 && L >= 17 && pts[0] != 0 && pts[1] != 0) {
+    const uint64_t r = h_mulmod(pts[1], h_invmod(pts[0], p), p);
+    bool ok = r != 1;
+    uint64_t cur = pts[1];
+    for (int t = 2; t < npts && ok; ++t) {
+      cur = h_mulmod(cur, r, p);
+      ok = cur == pts[t];
+    }
+    static const bool off = std::getenv("FPM_NO_CHIRP") != nullptr;
+    if (ok && !off)
+      return eval_points_geo(cx, (uint32_t)p, (const uint32_t*)P, L, L, (long long)m * n, a_dev,
+                             npts, GeoPts{true, (uint32_t)r, (uint32_t)h_invmod(r, p)},
+                             (uint32_t*)out);
+  }
   return eval_points(cx, (uint32_t)p, (const uint32_t*)P, L, L, (long long)m * n, a_dev, npts,
                      (uint32_t*)out);
 }
