@@ -22,7 +22,8 @@ using namespace nttp;
 // pair q (entries 2q, 2q+1) of twiddle row r is stored at pair q ^ sw(r)
 __device__ __forceinline__ int sw_row(int r) { return (r ^ (r >> 5)) & 7; }
 
-// v[i] *= row r [brev5(i)], pairs read from the swizzled smem table just in time
+// v[i] *= row r [brev5(i)], pairs read from the swizzled smem table just in
+// time; every value (row[0] = 1 also reduces the lazy outputs of dit_lazy)
 __device__ __forceinline__ void row_apply_s(uint32_t (&v)[32], const uint2* tws, int r,
                                             uint32_t p) {
   const uint4* base = reinterpret_cast<const uint4*>(tws + (size_t)r * 32);
@@ -31,7 +32,7 @@ __device__ __forceinline__ void row_apply_s(uint32_t (&v)[32], const uint2* tws,
   for (int q = 0; q < 16; ++q) {
     const uint4 t = base[q ^ s];
     const int k0 = 2 * q, k1 = 2 * q + 1;
-    if (k0) {
+    {
       const int i0 = brev5(k0);
       v[i0] = d_red(d_shoup(v[i0], t.x, t.y, p), p);
     }
@@ -65,11 +66,16 @@ __device__ __forceinline__ void fwd_passes(uint32_t (&v)[32], uint32_t* smt, con
                                            const PrimeConst& pc, int lt, bool upper_zero) {
   using G = Geo<LOGN, TPCX>;
   const uint32_t p = pc.p;
+  // radix passes as DIT on bit-reverse-aliased registers with lazy
+  // reductions (ntt_passes.cuh dit_lazy): the DIF network and placement
   if (G::NPASS == 1) {
-    dif_small<5>(v, pc.w32, p, false);
+    dit_lazy<5, true, false>(v, pc.w32, p);
     return;
   }
-  dif_small<5>(v, pc.w32, p, upper_zero);
+  if (upper_zero)
+    dit_lazy<5, true, true, true>(v, pc.w32, p);
+  else
+    dit_lazy<5, true, true>(v, pc.w32, p);
   row_apply_s(v, tws, lt, p);
   __syncthreads();
   to_smem<LOGN, MAP_TOP>(smt, v, lt);
@@ -77,14 +83,14 @@ __device__ __forceinline__ void fwd_passes(uint32_t (&v)[32], uint32_t* smt, con
     constexpr int lo = LOGN - 10;
     __syncthreads();
     from_smem<LOGN, MAP_MID>(smt, v, lt);
-    dif_small<5>(v, pc.w32, p, false);
+    dit_lazy<5, true, true>(v, pc.w32, p);
     row_apply_s(v, tws, (lt & ((1 << lo) - 1)) * 32, p);
     __syncthreads();
     to_smem<LOGN, MAP_MID>(smt, v, lt);
   }
   __syncthreads();
   from_smem<LOGN, MAP_LAST>(smt, v, lt);
-  dif_small<G::LAST_R>(v, pc.w32, p, false);
+  dit_lazy<G::LAST_R, true, false>(v, pc.w32, p);
 }
 
 template <int LOGN, int TPCX>
@@ -93,10 +99,10 @@ __device__ __forceinline__ void inv_passes(uint32_t (&v)[32], uint32_t* smt, con
   using G = Geo<LOGN, TPCX>;
   const uint32_t p = pc.p;
   if (G::NPASS == 1) {
-    dit_small<5>(v, pc.iw32, p);
+    dit_lazy<5, false, false>(v, pc.iw32, p);
     return;
   }
-  dit_small<G::LAST_R>(v, pc.iw32, p);
+  dit_lazy<G::LAST_R, false, true>(v, pc.iw32, p);  // the next pass multiplies every value
   __syncthreads();
   to_smem<LOGN, MAP_LAST>(smt, v, lt);
   __syncthreads();
@@ -104,14 +110,14 @@ __device__ __forceinline__ void inv_passes(uint32_t (&v)[32], uint32_t* smt, con
     constexpr int lo = LOGN - 10;
     from_smem<LOGN, MAP_MID>(smt, v, lt);
     row_apply_s(v, tws, (lt & ((1 << lo) - 1)) * 32, p);
-    dit_small<5>(v, pc.iw32, p);
+    dit_lazy<5, false, true>(v, pc.iw32, p);
     __syncthreads();
     to_smem<LOGN, MAP_MID>(smt, v, lt);
     __syncthreads();
   }
   from_smem<LOGN, MAP_TOP>(smt, v, lt);
   row_apply_s(v, tws, lt, p);
-  dit_small<5>(v, pc.iw32, p);
+  dit_lazy<5, false, false>(v, pc.iw32, p);
 }
 
 template <int THREADS>
