@@ -46,6 +46,7 @@ struct NttFwdArgs {
   int n_entries2;            // 0: none
   uint32_t* out2;
   long long out2_prime_stride;
+  int tma_pm;                // set by the persistent launcher: PM output by TMA stores
 };
 
 struct NttInvArgs {

@@ -10,10 +10,14 @@
 //     butterfly work instead of stalling it.
 // Forward: u32 input (no fold / no reduction), blocked-eval or point-major
 // output.  Inverse: blocked-eval or point-major input.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cstdlib>
+#include <mutex>
 
 #include "ntt.cuh"
 #include "ntt_passes.cuh"
+#include "tc_common.cuh"
 
 namespace fpm {
 namespace {
@@ -127,10 +131,15 @@ constexpr int min_blocks() {
 
 template <int LOGN, bool SINGLE, int TPCX>
 __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN, TPCX>::THREADS>())
-    ntt_fwd_persist(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps) {
+    ntt_fwd_persist(const __grid_constant__ NttFwdArgs a, const __grid_constant__ PrimeSet ps,
+                    const __grid_constant__ CUtensorMap om1, const __grid_constant__ CUtensorMap om2) {
   using G = Geo<LOGN, TPCX>;
   extern __shared__ __align__(16) uint32_t sm[];
   uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
+  // point-major output of 4 transforms per CTA by TMA: dense [N][4] staging
+  // after the twiddle table; the elected thread stores 256-point boxes
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  uint4* stage = reinterpret_cast<uint4*>(tws + G::N);
   const int z = SINGLE ? 0 : blockIdx.z;
   const PrimeConst& pc = ps.pr[z];
   const int tid = threadIdx.x;
@@ -230,6 +239,27 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
         for (int i = 0; i < 32; ++i)
           out[(long long)xmap<LOGN, MAP_LAST>(lt, i) * jn + e] = v[i];
       }
+    } else if (kTmaPm && a.pm && a.tma_pm) {
+      // 16-byte row pieces (4 entries of one point) leave through the TMA
+      // unit: the LSU would issue one 16-byte store per point and stall on
+      // its queue (ncu: long-scoreboard on the store address registers)
+      __syncthreads();
+      to_smem<LOGN, MAP_LAST>(smt, v, lt);
+      if (tid == 0) tc::bulk_wait_read0();  // previous group's stores have read the staging
+      __syncthreads();
+      for (int x = tid; x < G::N; x += G::THREADS)
+        stage[x] = make_uint4(sm[pad(x)], sm[G::STRIDE + pad(x)], sm[2 * G::STRIDE + pad(x)],
+                              sm[3 * G::STRIDE + pad(x)]);
+      tc::fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        const CUtensorMap* om = second ? &om2 : &om1;
+        const uint32_t sbase = tc::smem_u32(stage);
+#pragma unroll 1
+        for (int j = 0; j < G::N / 256; ++j)
+          tc::tma_store_3d(om, sbase + 4096u * j, (int)e0, 256 * j, z);
+        tc::bulk_commit();
+      }
     } else if (a.pm) {
       __syncthreads();
       to_smem<LOGN, MAP_LAST>(smt, v, lt);
@@ -266,6 +296,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     __syncthreads();  // smem exchange buffer reused by the next group
     if (!kPrefetch && nxt < groups) load_group(nxt);
   }
+  if (kTmaPm && a.tma_pm && tid == 0) tc::bulk_wait0();
 }
 
 template <int LOGN, bool SINGLE, int TPCX>
@@ -430,10 +461,53 @@ constexpr int pm_tpc2() {
   return (1 << LOGN) <= 2048 ? 0 : ((1 << LOGN) <= 4096 ? 4 : kPaired);
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 pm_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }
+  return fn;
+}
+
+// point-major evaluations E[z][t][entry]: boxes of 4 entries x 256 points
+bool pm_map(CUtensorMap* m, uint32_t* base, long long entries, int N, long long prime_stride,
+            int primes) {
+  auto fn = pm_encode_fn();
+  if (!fn || !base || ((uintptr_t)base & 15) || (entries & 3) || (prime_stride & 3)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)entries, (cuuint64_t)N, (cuuint64_t)primes};
+  const cuuint64_t strides[2] = {(cuuint64_t)entries * 4,
+                                 (cuuint64_t)(primes > 1 ? prime_stride : (long long)N * entries) * 4};
+  const cuuint32_t box[3] = {4, 256, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int LOGN, bool SINGLE, int TPCX, bool FWD, typename Args>
-int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
+int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
   using G = Geo<LOGN, TPCX>;
-  const size_t smem = (size_t)((G::TPC * G::STRIDE + 3) & ~3) * 4 + (size_t)G::N * 8;
+  Args a = a_in;
+  CUtensorMap om1{}, om2{};
+  constexpr bool kTmaPm = FWD && G::TPC == 4 && !G::PAIRED;
+  if constexpr (kTmaPm) {
+    static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
+    a.tma_pm = 0;
+    if (!off && a.pm && pm_map(&om1, a.out, a.n_entries, G::N, a.out_prime_stride, ps.count)) {
+      a.tma_pm = 1;
+      if (a.n_entries2 > 0)
+        a.tma_pm = pm_map(&om2, a.out2, a.n_entries2, G::N, a.out2_prime_stride, ps.count) ? 1 : 0;
+      else
+        om2 = om1;
+    }
+  }
+  const size_t smem = (size_t)((G::TPC * G::STRIDE + 3) & ~3) * 4 + (size_t)G::N * 8 +
+                      (kTmaPm ? (size_t)G::N * 16 : 0);
   const void* kern;
   if constexpr (FWD)
     kern = (const void*)ntt_fwd_persist<LOGN, SINGLE, TPCX>;
@@ -456,7 +530,8 @@ int persist_launch(const Args& a, const PrimeSet& ps, cudaStream_t st) {
   if (grid > groups) grid = groups;
   dim3 g3((unsigned)grid, 1, (unsigned)ps.count);
   if constexpr (FWD)
-    FPM_CUDA_TRY(launch_pdl(ntt_fwd_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps));
+    FPM_CUDA_TRY(launch_pdl(ntt_fwd_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps,
+                            om1, om2));
   else
     FPM_CUDA_TRY(launch_pdl(ntt_inv_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps));
   FPM_LAUNCH_CHECK();
