@@ -62,6 +62,7 @@ struct NttInvArgs {
   int out_len;
   int off;
   int scale;                 // multiply by N^-1 (1 for the product path)
+  int tma_pm;                // set by the persistent launcher: PM input by TMA loads
 };
 
 // host launchers (ntt.cu); LOGN in [5, 15]

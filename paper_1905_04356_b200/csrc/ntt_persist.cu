@@ -301,10 +301,17 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
 
 template <int LOGN, bool SINGLE, int TPCX>
 __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN, TPCX>::THREADS>())
-    ntt_inv_persist(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps) {
+    ntt_inv_persist(const __grid_constant__ NttInvArgs a, const __grid_constant__ PrimeSet ps,
+                    const __grid_constant__ CUtensorMap im) {
   using G = Geo<LOGN, TPCX>;
   extern __shared__ __align__(16) uint32_t sm[];
   uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
+  // point-major input of 4 transforms per CTA by TMA: 256-point boxes of 4
+  // entries land in a dense [N][4] staging tile a group ahead (mbarrier)
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  const bool tma_in = kTmaPm && a.pm && a.tma_pm;
+  uint4* stage = reinterpret_cast<uint4*>(tws + G::N);
+  uint64_t* mb = reinterpret_cast<uint64_t*>(stage + (kTmaPm ? G::N : 0));
   const int z = SINGLE ? 0 : blockIdx.z;
   const PrimeConst& pc = ps.pr[z];
   const uint32_t p = pc.p;
@@ -320,8 +327,21 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   constexpr int GQ = G::TPC / PW;
 
   stage_table<LOGN>(tws, pc.itw);
+  if (tma_in && tid == 0) {
+    tc::mbar_init(mb, 1);
+    tc::fence_mbar_init();
+    tc::prefetch_tmap(&im);
+  }
   pdl_wait();
   pdl_trigger();
+  auto tma_group = [&](long long g) {  // elected thread
+    tc::mbar_expect_tx(mb, (uint32_t)G::N * 16u);
+    const uint32_t sbase = tc::smem_u32(stage);
+#pragma unroll 1
+    for (int j = 0; j < G::N / 256; ++j)
+      tc::tma_load_3d(sbase + 4096u * j, &im, mb, (int)(g * G::TPC), 256 * j, z);
+  };
+  uint32_t phase = 0;
 
   uint32_t pre[32];
   auto load_group = [&](long long grp) {
@@ -389,12 +409,32 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   };
 
   long long grp = blockIdx.x;
-  if (grp < groups) load_group(grp);
+  if (grp < groups) {
+    if (tma_in) {
+      __syncthreads();  // barrier initialised
+      if (tid == 0) tma_group(grp);
+    } else {
+      load_group(grp);
+    }
+  }
   cp_async_wait_all();
   __syncthreads();  // table staged
   for (; grp < groups; grp += gridDim.x) {
     uint32_t v[32];
-    if (G::PAIRED && a.pm) {
+    if (tma_in) {
+      tc::mbar_wait(mb, phase);
+      phase ^= 1u;
+      for (int x = tid; x < G::N; x += G::THREADS) {
+        const uint4 t = stage[x];
+        sm[pad(x)] = t.x;
+        sm[G::STRIDE + pad(x)] = t.y;
+        sm[2 * G::STRIDE + pad(x)] = t.z;
+        sm[3 * G::STRIDE + pad(x)] = t.w;
+      }
+      __syncthreads();  // staging consumed: the next group may land
+      if (tid == 0 && grp + gridDim.x < groups) tma_group(grp + gridDim.x);
+      from_smem<LOGN, MAP_LAST>(smt, v, lt);
+    } else if (G::PAIRED && a.pm) {
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         // pre[i..i+1] = (T0, T1) at point i + tr; this lane wants T_tr at i, i+1
@@ -419,7 +459,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     }
     const long long nxt = grp + gridDim.x;
     constexpr bool kPrefetch = G::THREADS <= 512;
-    if (kPrefetch && nxt < groups) load_group(nxt);
+    if (!tma_in && kPrefetch && nxt < groups) load_group(nxt);
     inv_passes<LOGN, TPCX>(v, smt, tws, pc, lt);
     if (a.scale) {
 #pragma unroll
@@ -450,7 +490,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
       }
     }
     __syncthreads();
-    if (!kPrefetch && nxt < groups) load_group(nxt);
+    if (!tma_in && !kPrefetch && nxt < groups) load_group(nxt);
   }
 }
 
@@ -494,8 +534,14 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
   using G = Geo<LOGN, TPCX>;
   Args a = a_in;
   CUtensorMap om1{}, om2{};
-  constexpr bool kTmaPm = FWD && G::TPC == 4 && !G::PAIRED;
-  if constexpr (kTmaPm) {
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  if constexpr (kTmaPm && !FWD) {
+    static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
+    a.tma_pm = (!off && a.pm &&
+                pm_map(&om1, const_cast<uint32_t*>(a.in), a.n_entries, G::N, a.in_prime_stride,
+                       ps.count)) ? 1 : 0;
+  }
+  if constexpr (kTmaPm && FWD) {
     static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
     a.tma_pm = 0;
     if (!off && a.pm && pm_map(&om1, a.out, a.n_entries, G::N, a.out_prime_stride, ps.count)) {
@@ -507,7 +553,7 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
     }
   }
   const size_t smem = (size_t)((G::TPC * G::STRIDE + 3) & ~3) * 4 + (size_t)G::N * 8 +
-                      (kTmaPm ? (size_t)G::N * 16 : 0);
+                      (kTmaPm ? (size_t)G::N * 16 + 16 : 0);
   const void* kern;
   if constexpr (FWD)
     kern = (const void*)ntt_fwd_persist<LOGN, SINGLE, TPCX>;
@@ -533,7 +579,8 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
     FPM_CUDA_TRY(launch_pdl(ntt_fwd_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps,
                             om1, om2));
   else
-    FPM_CUDA_TRY(launch_pdl(ntt_inv_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps));
+    FPM_CUDA_TRY(launch_pdl(ntt_inv_persist<LOGN, SINGLE, TPCX>, dim3(g3), dim3(G::THREADS), smem, st, a, ps,
+                            om1));
   FPM_LAUNCH_CHECK();
   return kOk;
 }

@@ -189,6 +189,16 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// 3-D tiled TMA load global -> shared, completion on an mbarrier (tx bytes)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const void* tmap, uint64_t* mbar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(dst),
+      "l"(tmap), "r"(smem_u32(mbar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // TMA tensor store shared -> global (bulk group), and the group waits
 __device__ __forceinline__ void tma_store_3d(const void* tmap, uint32_t src, int c0, int c1,
                                              int c2) {
