@@ -136,9 +136,11 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   using G = Geo<LOGN, TPCX>;
   extern __shared__ __align__(16) uint32_t sm[];
   uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
-  // point-major output of 4 transforms per CTA by TMA: dense [N][4] staging
-  // after the twiddle table; the elected thread stores 256-point boxes
-  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  // point-major output of the TPC >= 4 transforms of a CTA by TMA: dense
+  // [N][TPC] staging after the twiddle table (TPC * N = 8192 words); the
+  // elected thread stores boxes of TPC entries x BP points
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;  // N = 2048, 4096 (measured: smaller N lose)
+  constexpr int BP = G::N < 256 ? G::N : 256;
   uint4* stage = reinterpret_cast<uint4*>(tws + G::N);
   const int z = SINGLE ? 0 : blockIdx.z;
   const PrimeConst& pc = ps.pr[z];
@@ -247,17 +249,21 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
       to_smem<LOGN, MAP_LAST>(smt, v, lt);
       if (tid == 0) tc::bulk_wait_read0();  // previous group's stores have read the staging
       __syncthreads();
-      for (int x = tid; x < G::N; x += G::THREADS)
-        stage[x] = make_uint4(sm[pad(x)], sm[G::STRIDE + pad(x)], sm[2 * G::STRIDE + pad(x)],
-                              sm[3 * G::STRIDE + pad(x)]);
+      constexpr int Q4 = G::TPC / 4;  // 16-byte chunks per point
+      for (int idx = tid; idx < G::N * Q4; idx += G::THREADS) {
+        const int x = idx / Q4, c = idx - (idx / Q4) * Q4;
+        stage[idx] = make_uint4(sm[(4 * c) * G::STRIDE + pad(x)], sm[(4 * c + 1) * G::STRIDE + pad(x)],
+                                sm[(4 * c + 2) * G::STRIDE + pad(x)],
+                                sm[(4 * c + 3) * G::STRIDE + pad(x)]);
+      }
       tc::fence_proxy_async();
       __syncthreads();
       if (tid == 0) {
         const CUtensorMap* om = second ? &om2 : &om1;
         const uint32_t sbase = tc::smem_u32(stage);
 #pragma unroll 1
-        for (int j = 0; j < G::N / 256; ++j)
-          tc::tma_store_3d(om, sbase + 4096u * j, (int)e0, 256 * j, z);
+        for (int j = 0; j < G::N / BP; ++j)
+          tc::tma_store_3d(om, sbase + (uint32_t)(BP * G::TPC * 4) * j, (int)e0, BP * j, z);
         tc::bulk_commit();
       }
     } else if (a.pm) {
@@ -306,12 +312,14 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   using G = Geo<LOGN, TPCX>;
   extern __shared__ __align__(16) uint32_t sm[];
   uint2* tws = reinterpret_cast<uint2*>(sm + ((G::TPC * G::STRIDE + 3) & ~3));
-  // point-major input of 4 transforms per CTA by TMA: 256-point boxes of 4
-  // entries land in a dense [N][4] staging tile a group ahead (mbarrier)
-  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  // point-major input of the TPC >= 4 transforms of a CTA by TMA: boxes of
+  // TPC entries x BP points land in a dense [N][TPC] staging tile a group
+  // ahead (mbarrier)
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;  // N = 2048, 4096 (measured: smaller N lose)
+  constexpr int BP = G::N < 256 ? G::N : 256;
   const bool tma_in = kTmaPm && a.pm && a.tma_pm;
   uint4* stage = reinterpret_cast<uint4*>(tws + G::N);
-  uint64_t* mb = reinterpret_cast<uint64_t*>(stage + (kTmaPm ? G::N : 0));
+  uint64_t* mb = reinterpret_cast<uint64_t*>(stage + (kTmaPm ? G::N * G::TPC / 4 : 0));
   const int z = SINGLE ? 0 : blockIdx.z;
   const PrimeConst& pc = ps.pr[z];
   const uint32_t p = pc.p;
@@ -335,11 +343,11 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   pdl_wait();
   pdl_trigger();
   auto tma_group = [&](long long g) {  // elected thread
-    tc::mbar_expect_tx(mb, (uint32_t)G::N * 16u);
+    tc::mbar_expect_tx(mb, (uint32_t)G::N * G::TPC * 4u);
     const uint32_t sbase = tc::smem_u32(stage);
 #pragma unroll 1
-    for (int j = 0; j < G::N / 256; ++j)
-      tc::tma_load_3d(sbase + 4096u * j, &im, mb, (int)(g * G::TPC), 256 * j, z);
+    for (int j = 0; j < G::N / BP; ++j)
+      tc::tma_load_3d(sbase + (uint32_t)(BP * G::TPC * 4) * j, &im, mb, (int)(g * G::TPC), BP * j, z);
   };
   uint32_t phase = 0;
 
@@ -424,12 +432,14 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     if (tma_in) {
       tc::mbar_wait(mb, phase);
       phase ^= 1u;
-      for (int x = tid; x < G::N; x += G::THREADS) {
-        const uint4 t = stage[x];
-        sm[pad(x)] = t.x;
-        sm[G::STRIDE + pad(x)] = t.y;
-        sm[2 * G::STRIDE + pad(x)] = t.z;
-        sm[3 * G::STRIDE + pad(x)] = t.w;
+      constexpr int Q4 = G::TPC / 4;
+      for (int idx = tid; idx < G::N * Q4; idx += G::THREADS) {
+        const int x = idx / Q4, c = idx - (idx / Q4) * Q4;
+        const uint4 t = stage[idx];
+        sm[(4 * c) * G::STRIDE + pad(x)] = t.x;
+        sm[(4 * c + 1) * G::STRIDE + pad(x)] = t.y;
+        sm[(4 * c + 2) * G::STRIDE + pad(x)] = t.z;
+        sm[(4 * c + 3) * G::STRIDE + pad(x)] = t.w;
       }
       __syncthreads();  // staging consumed: the next group may land
       if (tid == 0 && grp + gridDim.x < groups) tma_group(grp + gridDim.x);
@@ -516,13 +526,15 @@ PFN_cuTensorMapEncodeTiled_v12000 pm_encode_fn() {
 
 // point-major evaluations E[z][t][entry]: boxes of 4 entries x 256 points
 bool pm_map(CUtensorMap* m, uint32_t* base, long long entries, int N, long long prime_stride,
-            int primes) {
+            int primes, int tpc) {
   auto fn = pm_encode_fn();
-  if (!fn || !base || ((uintptr_t)base & 15) || (entries & 3) || (prime_stride & 3)) return false;
+  if (!fn || !base || ((uintptr_t)base & 15) || (entries & 3) || (prime_stride & 3) ||
+      (tpc & 3))
+    return false;
   const cuuint64_t dims[3] = {(cuuint64_t)entries, (cuuint64_t)N, (cuuint64_t)primes};
   const cuuint64_t strides[2] = {(cuuint64_t)entries * 4,
                                  (cuuint64_t)(primes > 1 ? prime_stride : (long long)N * entries) * 4};
-  const cuuint32_t box[3] = {4, 256, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)tpc, (cuuint32_t)(N < 256 ? N : 256), 1};
   const cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, base, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -534,26 +546,28 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
   using G = Geo<LOGN, TPCX>;
   Args a = a_in;
   CUtensorMap om1{}, om2{};
-  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;
+  constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;  // N = 2048, 4096 (measured: smaller N lose)
   if constexpr (kTmaPm && !FWD) {
     static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
     a.tma_pm = (!off && a.pm &&
                 pm_map(&om1, const_cast<uint32_t*>(a.in), a.n_entries, G::N, a.in_prime_stride,
-                       ps.count)) ? 1 : 0;
+                       ps.count, G::TPC)) ? 1 : 0;
   }
   if constexpr (kTmaPm && FWD) {
     static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
     a.tma_pm = 0;
-    if (!off && a.pm && pm_map(&om1, a.out, a.n_entries, G::N, a.out_prime_stride, ps.count)) {
+    if (!off && a.pm &&
+        pm_map(&om1, a.out, a.n_entries, G::N, a.out_prime_stride, ps.count, G::TPC)) {
       a.tma_pm = 1;
       if (a.n_entries2 > 0)
-        a.tma_pm = pm_map(&om2, a.out2, a.n_entries2, G::N, a.out2_prime_stride, ps.count) ? 1 : 0;
+        a.tma_pm =
+            pm_map(&om2, a.out2, a.n_entries2, G::N, a.out2_prime_stride, ps.count, G::TPC) ? 1 : 0;
       else
         om2 = om1;
     }
   }
   const size_t smem = (size_t)((G::TPC * G::STRIDE + 3) & ~3) * 4 + (size_t)G::N * 8 +
-                      (kTmaPm ? (size_t)G::N * 16 + 16 : 0);
+                      (kTmaPm ? (size_t)G::N * G::TPC * 4 + 16 : 0);
   const void* kern;
   if constexpr (FWD)
     kern = (const void*)ntt_fwd_persist<LOGN, SINGLE, TPCX>;
