@@ -569,23 +569,43 @@ int inv_launch(const NttInvArgs& f, const PrimeSet& ps, cudaStream_t st) {
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
+// variant 0: 512 threads per CTA; 1: 768 (FPM_NTT_TMA_THREADS=768);
+// 2: one group per CTA, for batches too small to give every SM two groups
+// (cfg1: latency, not throughput)
 template <int PL>
-int fwd_pl(int logn, bool big, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
+int fwd_pl(int logn, int var, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
   switch (logn) {
-    case 11: return big ? fwd_launch<11, 12, PL>(a, ps, st) : fwd_launch<11, 8, PL>(a, ps, st);
-    case 12: return big ? fwd_launch<12, 6, PL>(a, ps, st) : fwd_launch<12, 4, PL>(a, ps, st);
-    case 13: return big ? fwd_launch<13, 3, PL>(a, ps, st) : fwd_launch<13, 2, PL>(a, ps, st);
+    case 11:
+      return var == 2 ? fwd_launch<11, 1, PL>(a, ps, st)
+                      : var == 1 ? fwd_launch<11, 12, PL>(a, ps, st) : fwd_launch<11, 8, PL>(a, ps, st);
+    case 12:
+      return var == 2 ? fwd_launch<12, 1, PL>(a, ps, st)
+                      : var == 1 ? fwd_launch<12, 6, PL>(a, ps, st) : fwd_launch<12, 4, PL>(a, ps, st);
+    case 13:
+      return var == 2 ? fwd_launch<13, 1, PL>(a, ps, st)
+                      : var == 1 ? fwd_launch<13, 3, PL>(a, ps, st) : fwd_launch<13, 2, PL>(a, ps, st);
   }
   return kUnsupported;
 }
 template <int PL>
-int inv_pl(int logn, bool big, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
+int inv_pl(int logn, int var, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
   switch (logn) {
-    case 11: return big ? inv_launch<11, 12, PL>(a, ps, st) : inv_launch<11, 8, PL>(a, ps, st);
-    case 12: return big ? inv_launch<12, 6, PL>(a, ps, st) : inv_launch<12, 4, PL>(a, ps, st);
-    case 13: return big ? inv_launch<13, 3, PL>(a, ps, st) : inv_launch<13, 2, PL>(a, ps, st);
+    case 11:
+      return var == 2 ? inv_launch<11, 1, PL>(a, ps, st)
+                      : var == 1 ? inv_launch<11, 12, PL>(a, ps, st) : inv_launch<11, 8, PL>(a, ps, st);
+    case 12:
+      return var == 2 ? inv_launch<12, 1, PL>(a, ps, st)
+                      : var == 1 ? inv_launch<12, 6, PL>(a, ps, st) : inv_launch<12, 4, PL>(a, ps, st);
+    case 13:
+      return var == 2 ? inv_launch<13, 1, PL>(a, ps, st)
+                      : var == 1 ? inv_launch<13, 3, PL>(a, ps, st) : inv_launch<13, 2, PL>(a, ps, st);
   }
   return kUnsupported;
+}
+
+int small_batch(long long items, int primes) {
+  static const bool off = std::getenv("FPM_NTT_NO_SMALL") != nullptr;
+  return !off && items * primes <= 2LL * sm_count();
 }
 
 }  // namespace
@@ -617,14 +637,16 @@ bool ntt_tma_inv_ok(int logn, const NttInvArgs& a) {
 }
 
 int launch_ntt_fwd_tma(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  bool big = tma_threads() == 768;
-  if (big && logn == 13 && fwd_smem<13, 3>(a.len) > kMaxSmem) big = false;
-  return (a.pblk_log == 2) ? fwd_pl<2>(logn, big, a, ps, st) : fwd_pl<5>(logn, big, a, ps, st);
+  int var = tma_threads() == 768 ? 1 : 0;
+  if (var == 1 && logn == 13 && fwd_smem<13, 3>(a.len) > kMaxSmem) var = 0;
+  if (small_batch((long long)a.n_entries + (a.n_entries2 > 0 ? a.n_entries2 : 0), ps.count)) var = 2;
+  return (a.pblk_log == 2) ? fwd_pl<2>(logn, var, a, ps, st) : fwd_pl<5>(logn, var, a, ps, st);
 }
 
 int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  const bool big = tma_threads() == 768 && logn == 11;  // 3 groups of 2^12/2^13 do not fit
-  return (a.pblk_log == 2) ? inv_pl<2>(logn, big, a, ps, st) : inv_pl<5>(logn, big, a, ps, st);
+  int var = tma_threads() == 768 && logn == 11 ? 1 : 0;  // 3 groups of 2^12/2^13 do not fit
+  if (small_batch(a.n_entries, ps.count)) var = 2;
+  return (a.pblk_log == 2) ? inv_pl<2>(logn, var, a, ps, st) : inv_pl<5>(logn, var, a, ps, st);
 }
 
 }  // namespace fpm
