@@ -228,56 +228,71 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
     fail(cudaStreamWaitEvent(down, start, 0));
   }
   const int is64 = elem_bytes == 8;
-  std::vector<bool> a_up(R, false), b_up(R, false);
+  // one "landed" event per uploaded row block of A / column block of B: a
+  // block of C waits only for its own two factors
+  std::vector<cudaEvent_t> a_ev(R, nullptr), b_ev(R, nullptr);
   // each row block of A and column block of B is transformed once and its
   // evaluations reused by the other blocks of its row / column
   std::vector<EvalCache> ca(R), cb(R);
-  // blocks in shells of max(i, j): shell s adds A_s and B_s and 2s + 1
-  // computable blocks, so the copy-out stream starts after one block's
-  // inputs and is fed faster than row-major order feeds it
+  // blocks in shells of max(i, j): shell s uploads A_s, multiplies the blocks
+  // (s, j < s) that need only A_s and earlier columns, then uploads B_s and
+  // multiplies (i <= s, s).  The copy-out stream starts after one block's
+  // inputs and, within a shell, before its last upload has landed
   std::vector<std::pair<int, int>> order;
   for (int sh = 0; sh < R; ++sh) {
-    for (int j = 0; j <= sh; ++j) order.push_back({sh, j});
-    for (int i = 0; i < sh; ++i) order.push_back({i, sh});
+    for (int j = 0; j < sh; ++j) order.push_back({sh, j});
+    for (int i = 0; i <= sh; ++i) order.push_back({i, sh});
+  }
+  auto upload_a = [&](int i) {
+    const int i0 = lo(i, m), ib = lo(i + 1, m) - i0;
+    if (ib > 0)
+      fail(cudaMemcpyAsync(dA + esz * (size_t)i0 * k * la,
+                         (const unsigned char*)A + esz * (size_t)i0 * k * la,
+                         esz * (size_t)ib * k * la, cudaMemcpyHostToDevice, up));
+    a_ev[i] = ev();
+    fail(cudaEventRecord(a_ev[i], up));
+  };
+  auto upload_b = [&](int j) {
+    const int j0 = lo(j, n), jb = lo(j + 1, n) - j0;
+    if (jb > 0)
+      fail(cudaMemcpy2DAsync(dB + esz * (size_t)k * j0 * lb, esz * (size_t)jb * lb,
+                           (const unsigned char*)B + esz * (size_t)j0 * lb, esz * (size_t)n * lb,
+                           esz * (size_t)jb * lb, k, cudaMemcpyHostToDevice, up));
+    b_ev[j] = ev();
+    fail(cudaEventRecord(b_ev[j], up));
+  };
+  // every upload is queued before the first product: the copy-in engine never
+  // waits for the host loop below (which may block on the context stream)
+  for (const auto& b : order) {
+    if (!a_ev[b.first]) upload_a(b.first);
+    if (!b_ev[b.second]) upload_b(b.second);
   }
   for (size_t ob = 0; ob < order.size() && status == kOk; ++ob) {
     const int i = order[ob].first, j = order[ob].second;
     const int i0 = lo(i, m), i1 = lo(i + 1, m), ib = i1 - i0;
-    {
-      const int j0 = lo(j, n), j1 = lo(j + 1, n), jb = j1 - j0;
-      unsigned char* dAi = dA + esz * (size_t)i0 * k * la;
-      unsigned char* dBj = dB + esz * (size_t)k * j0 * lb;  // column block j, packed [k][jb][lb]
-      unsigned char* dCij = dC + esz * ((size_t)i0 * n + (size_t)ib * j0) * lc;  // packed [ib][jb][lc]
-      if (!a_up[i]) {
-        fail(cudaMemcpyAsync(dAi, (const unsigned char*)A + esz * (size_t)i0 * k * la,
-                             esz * (size_t)ib * k * la, cudaMemcpyHostToDevice, up));
-        a_up[i] = true;
-      }
-      if (!b_up[j]) {
-        fail(cudaMemcpy2DAsync(dBj, esz * (size_t)jb * lb,
-                               (const unsigned char*)B + esz * (size_t)j0 * lb, esz * (size_t)n * lb,
-                               esz * (size_t)jb * lb, k, cudaMemcpyHostToDevice, up));
-        b_up[j] = true;
-      }
-      cudaEvent_t landed = ev();
-      fail(cudaEventRecord(landed, up));
-      fail(cudaStreamWaitEvent(st, landed, 0));
-      if (status != kOk) break;
-      MatRef Ar{dAi, is64, la, la};
-      MatRef Br{dBj, is64, lb, lb};
-      OutRef Cr{dCij, is64, lc, lc};
-      const int s2 = polmat_mul_cached(cx, p, ib, k, jb, Ar, Br, Cr, &ca[i], &cb[j]);
-      if (s2 != kOk) {
-        status = s2;
-        break;
-      }
-      cudaEvent_t done = ev();
-      fail(cudaEventRecord(done, st));
-      fail(cudaStreamWaitEvent(down, done, 0));
-      fail(cudaMemcpy2DAsync((unsigned char*)C + esz * ((size_t)i0 * n + j0) * lc,
-                             esz * (size_t)n * lc, dCij, esz * (size_t)jb * lc,
-                             esz * (size_t)jb * lc, ib, cudaMemcpyDeviceToHost, down));
+    const int j0 = lo(j, n), j1 = lo(j + 1, n), jb = j1 - j0;
+    unsigned char* dAi = dA + esz * (size_t)i0 * k * la;
+    unsigned char* dBj = dB + esz * (size_t)k * j0 * lb;  // column block j, packed [k][jb][lb]
+    unsigned char* dCij = dC + esz * ((size_t)i0 * n + (size_t)ib * j0) * lc;  // packed [ib][jb][lc]
+    fail(cudaStreamWaitEvent(st, a_ev[i], 0));
+    fail(cudaStreamWaitEvent(st, b_ev[j], 0));
+    if (status != kOk) break;
+    MatRef Ar{dAi, is64, la, la};
+    MatRef Br{dBj, is64, lb, lb};
+    OutRef Cr{dCij, is64, lc, lc};
+    static const int diag = std::getenv("FPM_HOST_DIAG") ? std::atoi(std::getenv("FPM_HOST_DIAG")) : 0;
+    // diag 1 (profiling only, results invalid): copies without the products
+    const int s2 = diag == 1 ? kOk : polmat_mul_cached(cx, p, ib, k, jb, Ar, Br, Cr, &ca[i], &cb[j]);
+    if (s2 != kOk) {
+      status = s2;
+      break;
     }
+    cudaEvent_t done = ev();
+    fail(cudaEventRecord(done, st));
+    fail(cudaStreamWaitEvent(down, done, 0));
+    fail(cudaMemcpy2DAsync((unsigned char*)C + esz * ((size_t)i0 * n + j0) * lc,
+                           esz * (size_t)n * lc, dCij, esz * (size_t)jb * lc,
+                           esz * (size_t)jb * lc, ib, cudaMemcpyDeviceToHost, down));
   }
   // the workspace returns to the pool in the context stream's order
   cudaEvent_t fin = ev();
