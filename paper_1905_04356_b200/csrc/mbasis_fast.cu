@@ -119,8 +119,15 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
     v[u] = col < NC ? W[ord[col] * (NC + 1) + gi]
                     : (col < m ? W[klist[col - NC] * (NC + 1) + gi] : 0u);
   }
+  // once c >= 16, columns 0..15 (u = 0) of every row are final zeros except
+  // the diagonals of rows < 16, which each block only rescales by D 2^-32:
+  // u = 0 is skipped and the product of those factors kept in S (Montgomery
+  // form) for the final diagonal
+  uint32_t S = f.c32;
 #pragma unroll
   for (int c = 0; c < NC; c += 2) {
+    constexpr int kSkip = 16;
+    const int u0 = c >= kSkip ? 1 : 0;
     uint32_t* pb = pbuf + ((c >> 1) & 1) * 128;
     if (gi == c) {
 #pragma unroll
@@ -136,27 +143,34 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
     if (trace && c == 0 && tid == 0) trace[7] = clock64();
     const uint32_t x = __shfl_sync(0xffffffffu, v[c >> 4], c & 15, 16);
     const uint32_t y = __shfl_sync(0xffffffffu, v[(c + 1) >> 4], (c + 1) & 15, 16);
+    // the row factors al = x e - y d (even lanes), be = y a - x b (odd lanes),
+    // once per lane pair instead of both in every lane
+    const bool odd = gs & 1;
+    const uint32_t ab = redc_axby(odd ? y : x, odd ? a : e, odd ? x : y, odd ? b : d, f);
+    const uint32_t al = __shfl_sync(0xffffffffu, ab, 0, 16);
+    const uint32_t be = __shfl_sync(0xffffffffu, ab, 1, 16);
+    if (c >= kSkip) S = redc_mul(S, dl, f);
     uint32_t rc[4], rd[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = u0; u < 4; ++u) {
       rc[u] = pb[gs + 16 * u];
       rd[u] = pb[64 + gs + 16 * u];
     }
     if (gi == c) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = redc_axby(e, rc[u], b, rd[u], f);
+      for (int u = u0; u < 4; ++u) v[u] = redc_axby(e, rc[u], b, rd[u], f);
     } else if (gi == c + 1) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = redc_axby(a, rd[u], d, rc[u], f);
+      for (int u = u0; u < 4; ++u) v[u] = redc_axby(a, rd[u], d, rc[u], f);
     } else {
-      const uint32_t al = redc_axby(x, e, y, d, f), be = redc_axby(y, a, x, b, f);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = redc3(dl, v[u], al, rc[u], be, rd[u], f);
+      for (int u = u0; u < 4; ++u) v[u] = redc3(dl, v[u], al, rc[u], be, rd[u], f);
     }
   }
   if (trace && tid == 0) trace[6] = clock64();
   // d_q = M[q][q] from the row's own threads; every thread of row q inverts it
-  const uint32_t dq = __shfl_sync(0xffffffffu, (gi >> 4) ? v[1] : v[0], gi & 15, 16);
+  uint32_t dq = __shfl_sync(0xffffffffu, (gi >> 4) ? v[1] : v[0], gi & 15, 16);
+  if (NC > 16 && gi < 16) dq = redc_mul(dq, S, f);  // the skipped rescalings
   const uint32_t iq = invmod(dq, f);
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
