@@ -110,6 +110,8 @@ template <int NC>
 __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int* klist,
                             uint32_t* pbuf, const F31& f, uint32_t* Ct, uint32_t* recC,
                             unsigned long long* trace) {
+  static_assert(NC == 32, "16 threads x 4 columns per row, 64 columns");
+  static_assert(((NC / 2 - 1) & 1) == 1, "the last block uses pivot buffer 1");
   const int tid = threadIdx.x, gi = tid >> 4, gs = tid & 15;
   const int nk = m - NC;
   uint32_t v[4];
@@ -168,10 +170,18 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
     }
   }
   if (trace && tid == 0) trace[6] = clock64();
-  // d_q = M[q][q] from the row's own threads; every thread of row q inverts it
-  uint32_t dq = __shfl_sync(0xffffffffu, (gi >> 4) ? v[1] : v[0], gi & 15, 16);
-  if (NC > 16 && gi < 16) dq = redc_mul(dq, S, f);  // the skipped rescalings
-  const uint32_t iq = invmod(dq, f);
+  // d_q = M[q][q] (row q: lane q & 15, register q >> 4) is published in the
+  // pivot buffer the last block did not use; one warp inverts all NC of them
+  // (16 lanes per row inverting the same value cost 4x the issue slots)
+  if (gs == (gi & 15)) pbuf[gi] = (gi >> 4) ? v[1] : v[0];
+  __syncthreads();
+  if (tid < NC) {
+    uint32_t dq = pbuf[tid];
+    if (NC > 16 && tid < 16) dq = redc_mul(dq, S, f);  // the skipped rescalings
+    pbuf[64 + tid] = invmod(dq, f);
+  }
+  __syncthreads();
+  const uint32_t iq = pbuf[64 + gi];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int col = gs + 16 * u;
