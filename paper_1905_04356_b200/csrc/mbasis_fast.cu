@@ -252,6 +252,89 @@ __device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct,
   }
 }
 
+// Residual-list update of the pair path (m = 64, n = np = nk = 32) on the
+// int8 tensor cores with register-level mma.sync (m16n8k32, u8 x u8 -> s32,
+// 8 cycles per warp-mma per SMSP measured, tools/micro/imma.cu):
+// G_t[klist[kr]][j] += sum_q Ct[q][kr] G_t[plist[q]][j] for every t > k,
+// computed transposed (M = j, N = kr).  With K' = (q, b) (b = byte of G) and
+// S_b = 2^(8b) Ct mod p split into bytes r, the sum is sum_r 2^(8r) D_r,
+// D_r[j][kr] = sum_K' byte_b(G_t[plist[q]][j]) byte_r(S_b[q][kr]): the A
+// fragments are the raw residual words themselves, the B fragments (one kr
+// tile per warp, all four planes, 32 registers) are built once per step in
+// Apk (4 planes x 32 x 32 words, XOR-swizzled rows) and stay in registers.
+// D_r < 128 * 255^2 < 2^23, so sum_r 2^(8r) D_r + G < 2^49 is one d_red64.
+__device__ __forceinline__ int apk_idx(int r, int row, int q) {
+  return (r * 32 + row) * 32 + (q ^ ((row & 7) << 2));
+}
+__device__ __forceinline__ void mma_u8_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, "
+      "{%8, %9}, {%0, %1, %2, %3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ void residual_mma(uint32_t* G, const uint32_t* Ct, uint32_t* Apk,
+                             const long long* krow, const long long* prow, int k, int nt,
+                             size_t mn, const F31& f) {
+  {
+    const uint32_t c8 = 256u % f.p, c16 = (uint32_t)(65536ull % f.p),
+                   c24 = (uint32_t)((1ull << 24) % f.p);
+    for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
+      const int kr = idx >> 5, q = idx & 31;
+      const uint32_t c = Ct[q * 32 + kr];
+      const uint32_t sb[4] = {c, mulmod(c, c8, f), mulmod(c, c16, f), mulmod(c, c24, f)};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) w |= ((sb[b] >> (8 * r)) & 0xffu) << (8 * b);
+        Apk[apk_idx(r, kr, q)] = w;
+      }
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  const int nw = blockDim.x >> 5;          // 16: 4 kr tiles x 4 tile streams
+  const int nbk = warp & 3, sub = warp >> 2, nsub = nw >> 2;
+  const int kr_b = nbk * 8 + g;            // B fragment column n = g
+  uint32_t bf[4][4][2];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      bf[r][kk][0] = Apk[apk_idx(r, kr_b, kk * 8 + tig)];
+      bf[r][kk][1] = Apk[apk_idx(r, kr_b, kk * 8 + tig + 4)];
+    }
+  const int tiles = 2 * nt;  // (t, 16 columns j) per kr tile
+  for (int tile = sub; tile < tiles; tile += nsub) {
+    const int t = k + 1 + (tile >> 1), j0 = (tile & 1) * 16;
+    uint32_t* Gt = G + (size_t)t * mn;
+    int d[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) d[r][e] = 0;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const uint32_t* g0 = Gt + prow[kk * 8 + tig] + j0 + g;
+      const uint32_t* g1 = Gt + prow[kk * 8 + tig + 4] + j0 + g;
+      const uint32_t a0 = g0[0], a1 = g0[8], a2 = g1[0], a3 = g1[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) mma_u8_16832(d[r], a0, a1, a2, a3, bf[r][kk][0], bf[r][kk][1]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = j0 + g + (e >> 1) * 8, kr = nbk * 8 + tig * 2 + (e & 1);
+      uint32_t* dst = Gt + krow[kr] + j;
+      const uint64_t acc = (uint64_t)(uint32_t)d[0][e] + ((uint64_t)(uint32_t)d[1][e] << 8) +
+                           ((uint64_t)(uint32_t)d[2][e] << 16) +
+                           ((uint64_t)(uint32_t)d[3][e] << 24) + *dst;
+      *dst = d_red64(acc, f.p, f.mu);
+    }
+  }
+}
+
 struct StepArgs {
   const uint32_t* F;
   long long fs;
@@ -594,7 +677,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     for (int q = tid; q < np; q += kStepThreads) prow[q] = rowoff[plist[q]];
     for (int kr = tid; kr < nk; kr += kStepThreads) krow[kr] = rowoff[klist[kr]];
     __syncthreads();
-    if (((n | nk) & 3) == 0 && a.fold_k == 4) {
+    if (pairs_done && m == 64 && nk == 32 && np == 32) {
+      // X (the stride-(n+1) copy of R_k, 64 x 64 words) is free after the solve
+      if (T - k - 1 > 0) residual_mma(G, Ct, X, krow, prow, k, T - k - 1, mn, f);
+    } else if (((n | nk) & 3) == 0 && a.fold_k == 4) {
       const int nt = T - k - 1;
       if (nt <= 2)
         residual_tiles<1>(G, Ct, krow, prow, n, nk, np, k, nt, mn, f);
