@@ -285,11 +285,10 @@ __device__ void residual_mma(uint32_t* G, const uint32_t* Ct, uint32_t* Apk,
       const uint32_t c = Ct[q * 32 + kr];
       const uint32_t sb[4] = {c, mulmod(c, c8, f), mulmod(c, c16, f), mulmod(c, c24, f)};
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        uint32_t w = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) w |= ((sb[b] >> (8 * r)) & 0xffu) << (8 * b);
-        Apk[apk_idx(r, kr, q)] = w;
+      for (int r = 0; r < 4; ++r) {  // byte r of sb[0..3] (PRMT)
+        const uint32_t lo = __byte_perm(sb[0], sb[1], r | ((4 + r) << 4));
+        const uint32_t hi = __byte_perm(sb[2], sb[3], r | ((4 + r) << 4));
+        Apk[apk_idx(r, kr, q)] = __byte_perm(lo, hi, 0x5410);
       }
     }
   }

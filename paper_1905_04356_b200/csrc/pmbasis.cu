@@ -455,7 +455,8 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
   if (!is64 && p < (1ull << 31)) {
     // shared-memory leaves; order 8 balances the per-step residual-list
     // update (grows with the leaf order) against the tree's products
-    // (cfg4: T = 16 179 ms, T = 8 168 ms, T = 4 184 ms)
+    // (cfg4 with the tensor-core residual update, tools/pmb_T.py: T = 32
+    // 95.7 ms, 16 95.6, 12 93.7, 8 93.7)
     const int tf = mbasis_fast_max_order(m, n);
     static const int tmax = std::getenv("FPM_PMBASIS_TMAX") ? std::atoi(std::getenv("FPM_PMBASIS_TMAX")) : 8;
     const int tcap = tf < tmax ? tf : tmax;
