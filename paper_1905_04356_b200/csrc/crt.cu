@@ -1,5 +1,6 @@
 // crt.cu -- Garner CRT, generic-modulus middle product, degree helpers.
 #include "crt.cuh"
+#include <algorithm>
 #include <climits>
 
 namespace fpm {
@@ -24,35 +25,49 @@ __device__ __forceinline__ uint64_t d_addmod64(uint64_t a, uint64_t b, uint64_t 
 
 namespace {
 
-__global__ void crt_kernel(CrtArgs a) {
+// Garner over R primes, then X mod P = REDC(sum_i v_i Mmont_i): the 32 x 64
+// products are summed as one 128-bit value (< 8 * 2^31 * P < P 2^64) and
+// reduced once (Mmont_i = (prod_{j<i} q_j mod P) 2^64 mod P), instead of a
+// 64-bit Montgomery product per prime
+template <int R, typename I>
+__global__ void __launch_bounds__(256) crt_kernel(CrtArgs a) {
   pdl_wait();
-  const long long total = (long long)a.n_entries * a.len;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long e = idx / a.len;
-    const int t = (int)(idx - e * a.len);
+  // I = uint32_t when the index space fits: a 64-bit division per output
+  // is a long software sequence
+  const I total = (I)a.n_entries * (I)a.len, len = (I)a.len;
+  for (I idx = blockIdx.x * (I)blockDim.x + threadIdx.x; idx < total;
+       idx += (I)gridDim.x * blockDim.x) {
+    const I e = idx / len;
+    const int t = (int)(idx - e * len);
     const uint32_t* src = a.res + e * a.res_stride + t;
-    uint32_t v[kMaxPrimes];
+    uint32_t x0[R];
 #pragma unroll
-    for (int i = 0; i < kMaxPrimes; ++i) {
-      if (i >= a.r) break;
+    for (int i = 0; i < R; ++i) x0[i] = src[i * a.res_prime_stride];  // loads first
+    uint32_t v[R];
+    uint64_t lo = 0, hi = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
       const uint32_t qi = a.q[i];
-      uint32_t x = src[i * a.res_prime_stride];
+      uint32_t x = x0[i];
 #pragma unroll
-      for (int j = 0; j < kMaxPrimes; ++j) {
-        if (j >= i) break;
+      for (int j = 0; j < i; ++j) {
         const uint32_t vj = v[j] >= qi ? v[j] - qi : v[j];
         x = x - vj + qi;  // [1, 2 qi)
         x = d_red(d_shoup(x, a.g[j][i], a.gsh[j][i], qi), qi);
       }
       v[i] = x;
+      const uint64_t M = a.Mmont[i];
+      const uint64_t p0 = (uint64_t)x * (uint32_t)M;
+      const uint64_t p1 = (uint64_t)x * (uint32_t)(M >> 32);
+      lo += p0;
+      hi += lo < p0;
+      const uint64_t s1 = p1 << 32;
+      lo += s1;
+      hi += (lo < s1) + (p1 >> 32);
     }
-    uint64_t s = 0;
-#pragma unroll
-    for (int i = 0; i < kMaxPrimes; ++i) {
-      if (i >= a.r) break;
-      s = d_addmod64(s, d_montmul(v[i], a.Mmont[i], a.P, a.Pni), a.P);
-    }
+    const uint64_t mq = lo * a.Pni;
+    uint64_t s = hi + __umul64hi(mq, a.P) + (lo != 0);
+    s = s >= a.P ? s - a.P : s;
     if (a.out64)
       ((uint64_t*)a.out)[e * a.out_stride + t] = s;
     else
@@ -215,6 +230,19 @@ int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64
 }
 
 void crt_prepare(CrtArgs& a, const uint32_t* q, int r, uint64_t P) {
+  // the constants depend on (q, P) only: the last set is reused (per thread)
+  thread_local CrtArgs last{};
+  thread_local bool have = false;
+  if (have && last.r == r && last.P == P && std::equal(q, q + r, last.q)) {
+    a.r = r;
+    a.P = P;
+    a.Pni = last.Pni;
+    std::copy(last.q, last.q + kMaxPrimes, a.q);
+    std::copy(&last.g[0][0], &last.g[0][0] + kMaxPrimes * kMaxPrimes, &a.g[0][0]);
+    std::copy(&last.gsh[0][0], &last.gsh[0][0] + kMaxPrimes * kMaxPrimes, &a.gsh[0][0]);
+    std::copy(last.Mmont, last.Mmont + kMaxPrimes, a.Mmont);
+    return;
+  }
   a.r = r;
   for (int i = 0; i < r; ++i) a.q[i] = q[i];
   for (int i = 0; i < r; ++i)
@@ -234,16 +262,46 @@ void crt_prepare(CrtArgs& a, const uint32_t* q, int r, uint64_t P) {
     a.Mmont[i] = (uint64_t)((u128)prod * R % P);
     prod = h_mulmod(prod, q[i] % P, P);
   }
+  last = a;
+  have = true;
+}
+
+template <int R>
+int launch_crt_r(const CrtArgs& a, long long total, cudaStream_t st) {
+  // one resident wave (grid-stride loop): no partial last wave
+  static int per_sm = 0, sms = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, crt_kernel<R, uint32_t>, 256, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (per_sm < 1) per_sm = 1;
+    if (sms < 1) sms = 148;
+  }
+  long long blocks = (total + 255) / 256;
+  if (blocks > (long long)per_sm * sms) blocks = (long long)per_sm * sms;
+  if (total + (long long)blocks * 256 < (1LL << 32))
+    FPM_CUDA_TRY(launch_pdl(crt_kernel<R, uint32_t>, dim3((unsigned)blocks), dim3(256), 0, st, a));
+  else
+    FPM_CUDA_TRY(launch_pdl(crt_kernel<R, unsigned long long>, dim3((unsigned)blocks), dim3(256), 0, st, a));
+  FPM_LAUNCH_CHECK();
+  return kOk;
 }
 
 int launch_crt(const CrtArgs& a, cudaStream_t st) {
   const long long total = (long long)a.n_entries * a.len;
   if (total <= 0) return kOk;
-  long long blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  FPM_CUDA_TRY(launch_pdl(crt_kernel, dim3((unsigned)blocks), dim3(256), 0, st, a));
-  FPM_LAUNCH_CHECK();
-  return kOk;
+  static_assert(kMaxPrimes == 8, "crt_kernel instantiations");
+  switch (a.r) {
+    case 1: return launch_crt_r<1>(a, total, st);
+    case 2: return launch_crt_r<2>(a, total, st);
+    case 3: return launch_crt_r<3>(a, total, st);
+    case 4: return launch_crt_r<4>(a, total, st);
+    case 5: return launch_crt_r<5>(a, total, st);
+    case 6: return launch_crt_r<6>(a, total, st);
+    case 7: return launch_crt_r<7>(a, total, st);
+    case 8: return launch_crt_r<8>(a, total, st);
+  }
+  set_last_error("CRT over %d primes (1..%d supported)", a.r, kMaxPrimes);
+  return kInvalidArgument;
 }
 
 int launch_middle_entrywise(const MiddleEntryArgs& a, cudaStream_t st) {

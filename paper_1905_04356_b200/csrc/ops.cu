@@ -23,52 +23,57 @@ int ceil_log2_min1(long long need) {
 
 namespace {
 
+// the element kernels index with I = uint32_t when the index space fits (a
+// 64-bit division per element is a long software sequence)
+template <typename I>
 __global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* out,
                              long long out_stride, long long entries, int len) {
   pdl_wait();
-  const long long total = entries * len;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i / len;
-    const int t = (int)(i - e * len);
-    out[e * out_stride + t] = in[e * in_stride + t];
+  const I total = (I)entries * (I)len, l = (I)len;
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const I e = i / l;
+    const int t = (int)(i - e * l);
+    out[(long long)e * out_stride + t] = in[(long long)e * in_stride + t];
   }
 }
 
 // out[z][e][t] = in[e][t] mod prime z (u32), t < len: lets wide or unreduced
 // inputs use the persistent u32 NTT (one cheap streaming pass)
+template <typename I>
 __global__ void split_reduce_kernel(const void* in, int in64, int reduce, long long stride,
                                     long long entries, int len, const __grid_constant__ PrimeSet ps,
                                     uint32_t* out) {
   pdl_wait();
   const PrimeConst& pc = ps.pr[blockIdx.y];
-  const long long total = entries * len;
-  uint32_t* o = out + (long long)blockIdx.y * total;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i / len;
-    const long long src = e * stride + (i - e * len);
+  const I total = (I)entries * (I)len, l = (I)len;
+  uint32_t* o = out + (long long)blockIdx.y * (long long)total;
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const I e = i / l;
+    const long long src = (long long)e * stride + (long long)(i - e * l);
     const uint64_t raw = in64 ? ((const unsigned long long*)in)[src]
                               : (uint64_t)((const uint32_t*)in)[src];
     o[i] = reduce ? d_red64(raw, pc.p, pc.mu) : (uint32_t)raw;
   }
 }
 
+template <typename I>
 __global__ void zero_tail_kernel(void* out, int is64, long long stride, long long entries,
                                  int from, int to) {
   pdl_wait();
-  const int w = to - from;
-  const long long total = entries * w;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const long long e = i / w;
+  const I w = (I)(to - from);
+  const I total = (I)entries * w;
+  for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
+    const I e = i / w;
     const int t = from + (int)(i - e * w);
     if (is64)
-      ((uint64_t*)out)[e * stride + t] = 0;
+      ((uint64_t*)out)[(long long)e * stride + t] = 0;
     else
-      ((uint32_t*)out)[e * stride + t] = 0;
+      ((uint32_t*)out)[(long long)e * stride + t] = 0;
   }
 }
+
+// 32-bit indices when every index a grid-stride loop forms stays below 2^32
+bool idx32(long long total, unsigned grid) { return total + (long long)grid * 256 < (1LL << 32); }
 
 unsigned grid_for(long long total) {
   long long b = (total + 255) / 256;
@@ -79,8 +84,13 @@ unsigned grid_for(long long total) {
 
 int zero_out(OutRef C, long long entries, int from, int to, cudaStream_t st) {
   if (to <= from || entries <= 0) return kOk;
-  FPM_CUDA_TRY(launch_pdl(zero_tail_kernel, dim3(grid_for(entries * (to - from))), dim3(256), 0, st, C.ptr, C.is64, C.stride,
-                                                                   entries, from, to));
+  const unsigned g = grid_for(entries * (to - from));
+  if (idx32(entries * (to - from), g))
+    FPM_CUDA_TRY(launch_pdl(zero_tail_kernel<uint32_t>, dim3(g), dim3(256), 0, st, C.ptr, C.is64,
+                            C.stride, entries, from, to));
+  else
+    FPM_CUDA_TRY(launch_pdl(zero_tail_kernel<unsigned long long>, dim3(g), dim3(256), 0, st,
+                            C.ptr, C.is64, C.stride, entries, from, to));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -211,8 +221,12 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     uint32_t* buf;
     FPM_TRY(ws.get((size_t)r * entries * f.len, &buf));
     dim3 g((unsigned)grid_for(entries * f.len), (unsigned)r);
-    FPM_CUDA_TRY(launch_pdl(split_reduce_kernel, dim3(g), dim3(256), 0, st, f.in, f.in64, f.reduce, f.in_stride, entries, f.len,
-                                           ps, buf));
+    if (idx32(entries * f.len, g.x))
+      FPM_CUDA_TRY(launch_pdl(split_reduce_kernel<uint32_t>, dim3(g), dim3(256), 0, st, f.in,
+                              f.in64, f.reduce, f.in_stride, entries, f.len, ps, buf));
+    else
+      FPM_CUDA_TRY(launch_pdl(split_reduce_kernel<unsigned long long>, dim3(g), dim3(256), 0, st,
+                              f.in, f.in64, f.reduce, f.in_stride, entries, f.len, ps, buf));
     FPM_LAUNCH_CHECK();
     f.in = buf; f.in64 = 0; f.reduce = 0; f.in_stride = f.len;
     f.in_prime_stride = entries * f.len;
@@ -332,8 +346,13 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     }
     StageTimer t2_(cx, direct ? "widen" : "crt");
     if (direct) {
-      FPM_CUDA_TRY(launch_pdl(widen_kernel, dim3(grid_for(ec * wlen)), dim3(256), 0, st, R, wlen, (uint64_t*)C.ptr, C.stride,
-                                                      ec, wlen));
+      const unsigned g = grid_for(ec * wlen);
+      if (idx32(ec * wlen, g))
+        FPM_CUDA_TRY(launch_pdl(widen_kernel<uint32_t>, dim3(g), dim3(256), 0, st, R, wlen,
+                                (uint64_t*)C.ptr, C.stride, ec, wlen));
+      else
+        FPM_CUDA_TRY(launch_pdl(widen_kernel<unsigned long long>, dim3(g), dim3(256), 0, st, R,
+                                wlen, (uint64_t*)C.ptr, C.stride, ec, wlen));
       FPM_LAUNCH_CHECK();
     } else {
       CrtArgs ca{};
