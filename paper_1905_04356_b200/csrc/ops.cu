@@ -38,21 +38,25 @@ __global__ void widen_kernel(const uint32_t* in, long long in_stride, uint64_t* 
 }
 
 // out[z][e][t] = in[e][t] mod prime z (u32), t < len: lets wide or unreduced
-// inputs use the persistent u32 NTT (one cheap streaming pass)
+// inputs use the persistent u32 NTT (one cheap streaming pass; each input
+// word is read once and reduced into every prime's plane)
 template <typename I>
 __global__ void split_reduce_kernel(const void* in, int in64, int reduce, long long stride,
                                     long long entries, int len, const __grid_constant__ PrimeSet ps,
                                     uint32_t* out) {
   pdl_wait();
-  const PrimeConst& pc = ps.pr[blockIdx.y];
   const I total = (I)entries * (I)len, l = (I)len;
-  uint32_t* o = out + (long long)blockIdx.y * (long long)total;
   for (I i = blockIdx.x * (I)blockDim.x + threadIdx.x; i < total; i += (I)gridDim.x * blockDim.x) {
     const I e = i / l;
     const long long src = (long long)e * stride + (long long)(i - e * l);
     const uint64_t raw = in64 ? ((const unsigned long long*)in)[src]
                               : (uint64_t)((const uint32_t*)in)[src];
-    o[i] = reduce ? d_red64(raw, pc.p, pc.mu) : (uint32_t)raw;
+#pragma unroll
+    for (int z = 0; z < kMaxPrimes; ++z) {
+      if (z >= ps.count) break;
+      out[(long long)z * (long long)total + i] =
+          reduce ? d_red64(raw, ps.pr[z].p, ps.pr[z].mu) : (uint32_t)raw;
+    }
   }
 }
 
@@ -220,7 +224,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     if (!(f.in64 || f.reduce) || f.fold || f.len <= 0 || logn > 13) return kOk;
     uint32_t* buf;
     FPM_TRY(ws.get((size_t)r * entries * f.len, &buf));
-    dim3 g((unsigned)grid_for(entries * f.len), (unsigned)r);
+    dim3 g((unsigned)grid_for(entries * f.len), 1u);
     if (idx32(entries * f.len, g.x))
       FPM_CUDA_TRY(launch_pdl(split_reduce_kernel<uint32_t>, dim3(g), dim3(256), 0, st, f.in,
                               f.in64, f.reduce, f.in_stride, entries, f.len, ps, buf));
