@@ -281,3 +281,20 @@ def test_cfg5_full_size_properties():
         i, j = (int(v) for v in rng.integers(0, 256, 2))
         ref = O.pm_mul(p, An[i:i + 1], Bn[:, j:j + 1])
         assert np.array_equal(Cn[i:i + 1, j:j + 1], ref)
+
+
+@pytest.mark.parametrize("p", [(1 << 62) - 57, P60, (1 << 40) - 87])
+def test_pm_mul_multiprime_extremes(p):
+    """Multi-prime products at the top of the modulus range: the Garner
+    recombination sums the mixed-radix digits as one 128-bit value before a
+    single reduction (crt.cu), so all-(p-1) operands are the worst case."""
+    rng = np.random.default_rng(p % 1000)
+    for (m, k, n, la, lb, full) in [(3, 4, 2, 1500, 1300, False), (2, 5, 3, 700, 900, True)]:
+        if full:
+            A = np.full((m, k, la), p - 1, dtype=np.uint64)
+            B = np.full((k, n, lb), p - 1, dtype=np.uint64)
+        else:
+            A = rng.integers(0, p, size=(m, k, la), dtype=np.uint64)
+            B = rng.integers(0, p, size=(k, n, lb), dtype=np.uint64)
+        C = dense.pm_mul_dense(dense.to_device(A, p), dense.to_device(B, p), p)
+        assert np.array_equal(dense.to_numpy(C, p).astype(np.uint64), O.pm_mul(p, A, B)), (p, m, k, n)
