@@ -23,6 +23,12 @@
  *     is available from fpm_last_error() (thread-local).  Error codes map
  *     1:1 onto the reference exception classes (fpmat/errors.py).
  *   - Calls are deterministic: no result depends on atomics ordering.
+ *   - Device entry points are stream-ordered and return without waiting,
+ *     except where the reference's own dispatch needs a device value on the
+ *     host: fpm_polmat_middle / fpm_pm_middle_product read deg A and deg B
+ *     (one synchronisation, polmat.py:477-497) and fpm_mbasis / fpm_pmbasis
+ *     return *lp = deg P + 1 (one synchronisation at exit).  *_host entry
+ *     points return after their results are in host memory.
  */
 #ifndef FPMAT_B200_H
 #define FPMAT_B200_H
@@ -46,6 +52,7 @@ extern "C" {
 #define FPM_ERR_OUT_OF_RANGE 8        /* errors.OutOfRange      (modring.py:157-158) */
 #define FPM_ERR_COMPOSITE_MODULUS 9   /* errors.CompositeModulus (modring.py:159-160) */
 #define FPM_ERR_DUPLICATE_POINTS 10   /* errors.DuplicatePoints (appint.py:203-205) */
+#define FPM_ERR_NO_SUCH_ELEMENT 11    /* errors.NoSuchElement   (modring.py:195-196) */
 #define FPM_ERR_INVALID_ARGUMENT 20   /* ValueError */
 #define FPM_ERR_UNSUPPORTED 21        /* size outside the implemented kernels */
 #define FPM_ERR_CUDA 30
@@ -69,6 +76,17 @@ int fpm_context_synchronize(fpm_context* ctx);
  * two_adicity and the 2^k-order root (smallest QNR ^ ((p-1) >> k)).
  * FPM_ERR_OUT_OF_RANGE unless 2 < p < 2^62; FPM_ERR_COMPOSITE_MODULUS. */
 int fpm_field_info(uint64_t p, int* two_adicity, uint64_t* ntt_root);
+/* modring.is_prime (modring.py:25-47): 1 if n is prime (any n < 2^64) */
+int fpm_is_prime(uint64_t n);
+/* modring.factorize (modring.py:74-105): distinct primes ascending with
+ * exponents; *count = number of primes (FPM_ERR_INVALID_ARGUMENT if > cap) */
+int fpm_factorize(uint64_t n, uint64_t* primes, int* exps, int cap, int* count);
+/* FieldCtx.element_order (modring.py:131-148): order of a mod p, a != 0 */
+int fpm_element_order(uint64_t p, uint64_t a, uint64_t* order);
+/* modring.order_at_least (modring.py:186-201): the smallest a >= 2 of
+ * multiplicative order >= n (1 for n <= 1); FPM_ERR_NO_SUCH_ELEMENT when
+ * n > p - 1 */
+int fpm_order_at_least(uint64_t p, uint64_t n, uint64_t* a);
 
 /* ---- NTT (modring.ntt_forward / ntt_inverse, modring.py:272-286) --------
  * batch transforms of length 2^log_len, natural order in and out:
@@ -141,8 +159,10 @@ int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes,
 /* ---- interpolant bases (appint.m_intbasis / pm_intbasis,
  *      appint.py:208-319) --------------------------------------------------
  * E_dev: order constant matrices m x n, point-major [order][m][n]; alpha:
- * order host points (reduced mod p, pairwise distinct, else
- * FPM_ERR_DUPLICATE_POINTS); shift: m int64 (host).  P_dev receives the
+ * order host points as uint64 integers, pairwise distinct as integers like
+ * appint._check_points (appint.py:203-205; else FPM_ERR_DUPLICATE_POINTS),
+ * reduced mod p inside (1 and 1 + p are distinct points with one residue);
+ * shift: m int64 (host).  P_dev receives the
  * m x m s-ordered weak Popov interpolant basis with room for order+1
  * coefficients; *lp = deg(P)+1; rdeg_out (host, optional) = rdeg_s(P).
  * Pivot rows are multiplied by (x - alpha_k) (appint.py:79-117); the output
@@ -158,6 +178,13 @@ int fpm_m_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E_d
  * P_dev m x n of length L; npts host points; 31-bit primes, elem_bytes 4. */
 int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const void* P_dev,
                            int m, int n, int L, const uint64_t* pts, int npts, void* out_dev);
+
+/* Tuning / A-B switches of the kernel selection (no environment variable
+ * is read).  Defaults are the product configuration; name NULL resets all.
+ * Names: no_pdl, host_blocks, no_chirp, ntt_generic, ntt_no_tma,
+ * ntt_no_small, ntt_pm_lsu, ntt_pm_scatter, pmbasis_leaf, pmbasis_host_sync.
+ * FPM_ERR_INVALID_ARGUMENT for an unknown name. */
+int fpm_set_option(const char* name, long long value);
 
 /* base-case threshold used by fpm_pmbasis (default 32, config.py:18) */
 int fpm_set_pmbasis_threshold(fpm_context* ctx, int T);

@@ -21,7 +21,6 @@ from .polmat import (  # noqa: F401
     random_polmat,
 )
 from .appint import eval_polmat_points, m_intbasis, mbasis, mbasis1, pm_intbasis, pmbasis  # noqa: F401
-from . import fraction, kernel  # noqa: F401,E402  (callers one level up)
 
 __all__ = [
     "FieldCtx", "NttPlan", "field_new", "cached_field", "ntt_forward", "ntt_inverse",

@@ -14,10 +14,15 @@ from . import errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfpm_b200.so")
+# test-only build: the product objects plus the tensor-core self-test hooks
+# (csrc/tc_selftest.cu); never loaded by the package itself
+SELFTEST_PATH = os.path.join(_HERE, "libfpm_b200_selftest.so")
 
 _lock = threading.Lock()
 _lib = None
 _ctx = {}
+_st_lib = None
+_st_ctx = {}
 
 
 class FpmBackendError(RuntimeError):
@@ -35,6 +40,7 @@ _STATUS = {
     8: errors.OutOfRange,
     9: errors.CompositeModulus,
     10: errors.DuplicatePoints,
+    11: errors.NoSuchElement,
     20: ValueError,
     21: NotImplementedError,
 }
@@ -75,6 +81,10 @@ def lib():
             "fpm_context_set_stream": (i32, [vp, vp]),
             "fpm_context_synchronize": (i32, [vp]),
             "fpm_field_info": (i32, [u64, pint, ctypes.POINTER(ctypes.c_uint64)]),
+            "fpm_is_prime": (i32, [u64]),
+            "fpm_factorize": (i32, [u64, ctypes.POINTER(ctypes.c_uint64), pint, i32, pint]),
+            "fpm_element_order": (i32, [u64, u64, ctypes.POINTER(ctypes.c_uint64)]),
+            "fpm_order_at_least": (i32, [u64, u64, ctypes.POINTER(ctypes.c_uint64)]),
             "fpm_ntt_u32": (i32, [vp, u32, i32, i32, vp, vp, i32]),
             "fpm_ntt_u64": (i32, [vp, u64, i32, i32, vp, vp, i32]),
             "fpm_polmat_mul": (i32, [vp, u64, i32, vp, i32, i32, i32, vp, i32, i32, vp]),
@@ -88,6 +98,7 @@ def lib():
             "fpm_pmbasis_host": (i32, [vp, u64, i32, vp, i32, i32, i32, i32, pi64, vp, pint,
                                        pi64]),
             "fpm_set_pmbasis_threshold": (i32, [vp, i32]),
+            "fpm_set_option": (i32, [ctypes.c_char_p, i64]),
             "fpm_pm_intbasis": (i32, [vp, u64, i32, vp, i32, i32, i32,
                                       ctypes.POINTER(ctypes.c_uint64), pi64, vp, pint, pi64]),
             "fpm_m_intbasis": (i32, [vp, u64, i32, vp, i32, i32, i32,
@@ -181,3 +192,46 @@ def profile_records(h):
 
 def launch_count():
     return int(lib().fpm_launch_count())
+
+
+def set_option(name, value):
+    """fpm_set_option: kernel-selection switches for A/B measurements
+    (include/fpmat_b200.h); name None resets every option."""
+    check(lib().fpm_set_option(None if name is None else name.encode(), int(value)),
+          "fpm_set_option")
+
+
+def selftest_lib():
+    """The test-only library (tensor-core kernels called directly)."""
+    global _st_lib
+    with _lock:
+        if _st_lib is None:
+            if not os.path.exists(SELFTEST_PATH):
+                raise FpmBackendError(f"{SELFTEST_PATH} not built")
+            L = ctypes.CDLL(SELFTEST_PATH)
+            L.fpm_context_create.restype = ctypes.c_int
+            L.fpm_context_create.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+            L.fpm_context_set_stream.restype = ctypes.c_int
+            L.fpm_context_set_stream.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+            _st_lib = L
+    return _st_lib
+
+
+def selftest_context(device=0):
+    """A context of the self-test library on torch's current stream."""
+    import torch
+
+    L = selftest_lib()
+    with _lock:
+        h = _st_ctx.get(device)
+        if h is None:
+            hp = ctypes.c_void_p()
+            with torch.cuda.device(device):
+                rc = L.fpm_context_create(device, ctypes.byref(hp))
+            if rc != 0:
+                raise FpmBackendError(f"selftest fpm_context_create: status {rc}")
+            h = _st_ctx[device] = hp
+    rc = L.fpm_context_set_stream(h, ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream))
+    if rc != 0:
+        raise FpmBackendError(f"selftest fpm_context_set_stream: status {rc}")
+    return h

@@ -41,10 +41,18 @@ int check_dims(int m, int k, int n) {
   return kOk;
 }
 
-struct HostStage {
-  Workspace ws;
-  explicit HostStage(Context& cx) : ws(cx) {}
-};
+// every entry point runs on its context's device, whatever the calling
+// thread's current device is (tensors on cuda:1 with cuda:0 current)
+int bind_device(fpm_context* ctx) {
+  if (!ctx) {
+    set_last_error("null context");
+    return kInvalidArgument;
+  }
+  int cur = -1;
+  FPM_CUDA_TRY(cudaGetDevice(&cur));
+  if (cur != ctx->cx->device()) FPM_CUDA_TRY(cudaSetDevice(ctx->cx->device()));
+  return kOk;
+}
 
 }  // namespace
 
@@ -76,12 +84,12 @@ void fpm_context_destroy(fpm_context* ctx) {
 }
 
 int fpm_context_set_stream(fpm_context* ctx, void* stream) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   return ctx->cx->set_stream((cudaStream_t)stream);
 }
 
 int fpm_context_synchronize(fpm_context* ctx) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
   return kOk;
 }
@@ -100,9 +108,66 @@ int fpm_field_info(uint64_t p, int* two_adicity, uint64_t* root) {
   return kOk;
 }
 
+int fpm_is_prime(uint64_t n) { return h_is_prime(n) ? 1 : 0; }
+
+int fpm_factorize(uint64_t n, uint64_t* primes, int* exps, int cap, int* count) {
+  if (!count || cap < 0 || (cap > 0 && (!primes || !exps))) return kInvalidArgument;
+  if (n == 0) {
+    set_last_error("cannot factorise 0");
+    return kInvalidArgument;
+  }
+  const auto fac = h_factorize(n);
+  *count = (int)fac.size();
+  if ((int)fac.size() > cap) {
+    set_last_error("%d prime factors, room for %d", (int)fac.size(), cap);
+    return kInvalidArgument;
+  }
+  int i = 0;
+  for (const auto& qe : fac) {
+    primes[i] = qe.first;
+    exps[i] = qe.second;
+    ++i;
+  }
+  return kOk;
+}
+
+int fpm_element_order(uint64_t p, uint64_t a, uint64_t* order) {
+  if (!order) return kInvalidArgument;
+  FPM_TRY(fpm_field_info(p, nullptr, nullptr));
+  if (a % p == 0) {
+    set_last_error("0 has no multiplicative order");
+    return kInvalidArgument;
+  }
+  *order = h_element_order(p, a % p, h_factorize(p - 1));
+  return kOk;
+}
+
+int fpm_order_at_least(uint64_t p, uint64_t n, uint64_t* a) {
+  if (!a) return kInvalidArgument;
+  FPM_TRY(fpm_field_info(p, nullptr, nullptr));
+  if (n > p - 1) {
+    set_last_error("group order is %llu, no element of order %llu", (unsigned long long)(p - 1),
+                   (unsigned long long)n);
+    return kNoSuchElement;
+  }
+  if (n <= 1) {
+    *a = 1;
+    return kOk;
+  }
+  // deterministic scan 2, 3, ... (a generator exists, so this terminates)
+  const auto fac = h_factorize(p - 1);
+  for (uint64_t c = 2; c < p; ++c)
+    if (h_element_order(p, c, fac) >= n) {
+      *a = c;
+      return kOk;
+    }
+  set_last_error("no element of order >= %llu", (unsigned long long)n);
+  return kNoSuchElement;
+}
+
 int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch, const uint32_t* in,
                 uint32_t* out, int inverse) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   if (p >= (1u << 31) || p <= 2) {
     set_last_error("fpm_ntt_u32 needs 2 < p < 2^31");
     return kOutOfRange;
@@ -133,7 +198,7 @@ int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch, const uint
 
 int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch, const uint64_t* in,
                 uint64_t* out, int inverse) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   if (p <= 2 || p >= (1ull << 62)) {
     set_last_error("modulus must satisfy 2 < p < 2^62");
     return kOutOfRange;
@@ -159,7 +224,7 @@ int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch, const uint
 
 int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m, int k,
                    int la, const void* B, int n, int lb, void* C) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   FPM_TRY(check_elem(p, elem_bytes));
   FPM_TRY(check_dims(m, k, n));
   const int is64 = elem_bytes == 8;
@@ -178,7 +243,7 @@ int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, 
 // and the kernels instead of running as three serial phases.
 int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
                         int k, int la, const void* B, int n, int lb, void* C) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   FPM_TRY(check_elem(p, elem_bytes));
   FPM_TRY(check_dims(m, k, n));
   Context& cx = *ctx->cx;
@@ -191,7 +256,7 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   FPM_TRY(ws.get(esz * na + 1, &dA));
   FPM_TRY(ws.get(esz * nb + 1, &dB));
   FPM_TRY(ws.get(esz * nc + 1, &dC));
-  static const int force = std::getenv("FPM_HOST_BLOCKS") ? std::atoi(std::getenv("FPM_HOST_BLOCKS")) : 0;
+  const int force = (int)option(kOptHostBlocks);
   int R = force > 0 ? force : (esz * nc >= (256u << 20) ? 4 : esz * nc >= (8u << 20) ? 3 : 1);
   if (R > m) R = m;
   if (R > n) R = n;
@@ -267,6 +332,8 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
     if (!a_ev[b.first]) upload_a(b.first);
     if (!b_ev[b.second]) upload_b(b.second);
   }
+  cudaEvent_t up_done = ev();
+  fail(cudaEventRecord(up_done, up));
   for (size_t ob = 0; ob < order.size() && status == kOk; ++ob) {
     const int i = order[ob].first, j = order[ob].second;
     const int i0 = lo(i, m), i1 = lo(i + 1, m), ib = i1 - i0;
@@ -280,9 +347,7 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
     MatRef Ar{dAi, is64, la, la};
     MatRef Br{dBj, is64, lb, lb};
     OutRef Cr{dCij, is64, lc, lc};
-    static const int diag = std::getenv("FPM_HOST_DIAG") ? std::atoi(std::getenv("FPM_HOST_DIAG")) : 0;
-    // diag 1 (profiling only, results invalid): copies without the products
-    const int s2 = diag == 1 ? kOk : polmat_mul_cached(cx, p, ib, k, jb, Ar, Br, Cr, &ca[i], &cb[j]);
+    const int s2 = polmat_mul_cached(cx, p, ib, k, jb, Ar, Br, Cr, &ca[i], &cb[j]);
     if (s2 != kOk) {
       status = s2;
       break;
@@ -294,10 +359,13 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
                            esz * (size_t)n * lc, dCij, esz * (size_t)jb * lc,
                            esz * (size_t)jb * lc, ib, cudaMemcpyDeviceToHost, down));
   }
-  // the workspace returns to the pool in the context stream's order
+  // the workspace returns to the pool in the context stream's order, and no
+  // copy may still read the caller's buffers: join both copy streams on
+  // every exit path (an early product failure leaves uploads queued)
   cudaEvent_t fin = ev();
   fail(cudaEventRecord(fin, down));
   fail(cudaStreamWaitEvent(st, fin, 0));
+  fail(cudaStreamWaitEvent(st, up_done, 0));
   fail(cudaStreamSynchronize(st));
   for (auto e : evs) cx.give_event(e);
   for (auto& c : ca)
@@ -318,7 +386,8 @@ struct fpm_multiplier {
 int fpm_multiplier_create(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
                           int k, int la, int max_rhs_len, fpm_multiplier** out) {
   using namespace fpm;
-  if (!ctx || !out) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (!out) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   FPM_TRY(check_dims(m, k, 0));
   if (la < 0 || max_rhs_len < 1) {
@@ -353,6 +422,7 @@ int fpm_multiplier_create(fpm_context* ctx, uint64_t p, int elem_bytes, const vo
 int fpm_multiplier_apply(fpm_multiplier* mu, const void* B, int n, int lb, void* C) {
   using namespace fpm;
   if (!mu) return kInvalidArgument;
+  FPM_TRY(bind_device(mu->ctx));
   FPM_TRY(check_dims(mu->m, mu->k, n));
   if (lb > mu->max_rhs_len) {
     set_last_error("deg B = %d exceeds the multiplier envelope %d", lb - 1,
@@ -383,7 +453,7 @@ void fpm_multiplier_destroy(fpm_multiplier* mu) {
 int fpm_polmat_middle(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m,
                       int k, int la, const void* B, int n, int lb, long long c, int d, int exact,
                       void* R) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   FPM_TRY(check_elem(p, elem_bytes));
   FPM_TRY(check_dims(m, k, n));
   if (d <= 0) return kOk;
@@ -394,8 +464,7 @@ int fpm_polmat_middle(fpm_context* ctx, uint64_t p, int elem_bytes, const void* 
   Context& cx = *ctx->cx;
   const int is64 = elem_bytes == 8;
   int da = -1, db = -1;
-  FPM_TRY(matrix_degree(cx, A, is64, (long long)m * k, la, &da));
-  FPM_TRY(matrix_degree(cx, B, is64, (long long)k * n, lb, &db));
+  FPM_TRY(matrix_degrees(cx, A, is64, (long long)m * k, la, B, (long long)k * n, lb, &da, &db));
   MatRef Ar{A, is64, la, la};
   MatRef Br{B, is64, lb, lb};
   OutRef Rr{R, is64, d, d};
@@ -406,13 +475,12 @@ int fpm_pm_middle_product(fpm_context* ctx, uint64_t p, int elem_bytes, const vo
                           int k, int la, const void* B, int n, int lb, long long c, int d,
                           void* R) {
   // polmat.pm_middle_product contract (polmat.py:476-481)
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   FPM_TRY(check_elem(p, elem_bytes));
   Context& cx = *ctx->cx;
   const int is64 = elem_bytes == 8;
   int da = -1, db = -1;
-  FPM_TRY(matrix_degree(cx, A, is64, (long long)m * k, la, &da));
-  FPM_TRY(matrix_degree(cx, B, is64, (long long)k * n, lb, &db));
+  FPM_TRY(matrix_degrees(cx, A, is64, (long long)m * k, la, B, (long long)k * n, lb, &da, &db));
   if (da >= c && c > 0) {
     set_last_error("deg A = %d must be < c = %lld", da, c);
     return kDegreeTooLarge;
@@ -426,7 +494,8 @@ int fpm_pm_middle_product(fpm_context* ctx, uint64_t p, int elem_bytes, const vo
 
 int fpm_mbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n, int lf,
                int order, const int64_t* shift, void* P, int* lp, int64_t* rdeg_out) {
-  if (!ctx || !lp || (m > 0 && !shift)) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (!lp || (m > 0 && !shift)) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   if (m <= 0 || n < 0 || order < 0) {
     set_last_error("mbasis needs m >= 1, n >= 0, order >= 0");
@@ -440,7 +509,8 @@ int fpm_mbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int 
 
 int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n,
                 int lf, int order, const int64_t* shift, void* P, int* lp, int64_t* rdeg_out) {
-  if (!ctx || !lp || (m > 0 && !shift)) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (!lp || (m > 0 && !shift)) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   if (m <= 0 || n < 0 || order < 0) {
     set_last_error("pmbasis needs m >= 1, n >= 0, order >= 0");
@@ -453,7 +523,8 @@ int fpm_pmbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int
 int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F, int m, int n,
                      int lf, int order, const int64_t* shift, void* P, int* lp,
                      int64_t* rdeg_out) {
-  if (!ctx || !lp) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (!lp || (m > 0 && !shift)) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   if (m <= 0 || n < 0 || order < 0 || lf < 0) {
     set_last_error("pmbasis needs m >= 1, n >= 0, order >= 0");
@@ -476,7 +547,8 @@ int fpm_pmbasis_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void* F
 int fpm_pm_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E, int m, int n,
                     int order, const uint64_t* alpha, const int64_t* shift, void* P, int* lp,
                     int64_t* rdeg_out) {
-  if (!ctx || !lp || (m > 0 && !shift) || (order > 0 && (!alpha || !E))) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (!lp || (m > 0 && !shift) || (order > 0 && (!alpha || !E))) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   if (m <= 0 || n < 0 || order < 0) {
     set_last_error("intbasis needs m >= 1, n >= 0, order >= 0");
@@ -499,7 +571,8 @@ int fpm_m_intbasis(fpm_context* ctx, uint64_t p, int elem_bytes, const void* E, 
 
 int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const void* P, int m,
                            int n, int L, const uint64_t* pts, int npts, void* out) {
-  if (!ctx || m < 0 || n < 0 || L < 0 || npts < 0 || (npts > 0 && !pts)) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
+  if (m < 0 || n < 0 || L < 0 || npts < 0 || (npts > 0 && !pts)) return kInvalidArgument;
   FPM_TRY(check_elem(p, elem_bytes));
   if (elem_bytes != 4) {
     set_last_error("point evaluation takes uint32 operands (31-bit primes)");
@@ -509,7 +582,7 @@ int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const v
 }
 
 int fpm_profile_enable(fpm_context* ctx, int on) {
-  if (!ctx) return kInvalidArgument;
+  FPM_TRY(bind_device(ctx));
   ctx->cx->profile_enable(on != 0);
   return kOk;
 }
@@ -524,6 +597,8 @@ int fpm_profile_get(fpm_context* ctx, int i, char* name, int name_len, float* ms
   name[name_len - 1] = 0;
   return kOk;
 }
+
+int fpm_set_option(const char* name, long long value) { return set_option(name, value); }
 
 int fpm_set_pmbasis_threshold(fpm_context* ctx, int T) {
   if (!ctx || T < 1) return kInvalidArgument;

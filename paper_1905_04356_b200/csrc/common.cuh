@@ -30,6 +30,7 @@ enum Status : int {
   kOutOfRange = 8,
   kCompositeModulus = 9,
   kDuplicatePoints = 10,
+  kNoSuchElement = 11,
   kInvalidArgument = 20,
   kUnsupported = 21,
   kCudaError = 30,
@@ -91,6 +92,12 @@ static inline uint32_t h_shoup(uint32_t w, uint32_t p) {
 bool h_is_prime(uint64_t n);          // deterministic Miller-Rabin (modring.py:25-47)
 int h_two_adicity(uint64_t p);        // modring.py:161-165
 uint64_t h_ntt_root(uint64_t p);      // smallest QNR ^ ((p-1) >> k), modring.py:166-170
+}  // namespace fpm
+#include <map>
+namespace fpm {
+std::map<uint64_t, int> h_factorize(uint64_t n);  // {prime: exponent}, modring.py:74-105
+// multiplicative order of a mod p given the factorisation of p - 1
+uint64_t h_element_order(uint64_t p, uint64_t a, const std::map<uint64_t, int>& fac);
 
 // ---- device helpers ---------------------------------------------------------
 __device__ __forceinline__ uint32_t d_red(uint32_t x, uint32_t p) {
@@ -132,7 +139,24 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
-bool pdl_enabled();  // runtime.cu: off under FPM_NO_PDL
+// Tuning / A-B switches (fpm_set_option, include/fpmat_b200.h).  The
+// defaults are the product configuration; nothing reads the environment.
+enum Option : int {
+  kOptNoPdl = 0,          // "no_pdl": plain launches instead of PDL
+  kOptHostBlocks,         // "host_blocks": force R x R blocks in fpm_polmat_mul_host
+  kOptNoChirp,            // "no_chirp": Horner instead of chirp evaluation (intbasis)
+  kOptNttGeneric,         // "ntt_generic": generic single-CTA NTT kernels only
+  kOptNttNoTma,           // "ntt_no_tma": skip the grouped TMA NTT
+  kOptNttNoSmall,         // "ntt_no_small": no one-group-per-CTA variant
+  kOptNttPmLsu,           // "ntt_pm_lsu": point-major pieces by LSU stores, not TMA
+  kOptNttPmScatter,       // "ntt_pm_scatter": one transform per CTA in PM layout
+  kOptPmbasisLeaf,        // "pmbasis_leaf": cap of the device leaf order (default 8)
+  kOptPmbasisHostSync,    // "pmbasis_host_sync": host-synchronised recursion
+  kOptCount
+};
+long long option(Option o);
+int set_option(const char* name, long long value);
+bool pdl_enabled();  // option no_pdl
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,

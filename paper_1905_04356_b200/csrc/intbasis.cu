@@ -297,11 +297,12 @@ int intbasis_run(Context& cx, uint64_t p, const void* E, int m, int n, int order
                    (unsigned long long)p);
     return kUnsupported;
   }
-  // appint._check_points: pairwise distinct points (as field elements)
+  // appint._check_points (appint.py:203-205) compares the integers as given,
+  // not their residues: [1, 1 + p] is accepted and runs with a repeated point
   std::vector<uint32_t> pts(order);
   for (int t = 0; t < order; ++t) pts[t] = (uint32_t)(alpha_host[t] % p);
   {
-    std::vector<uint32_t> srt(pts);
+    std::vector<uint64_t> srt(alpha_host, alpha_host + order);
     std::sort(srt.begin(), srt.end());
     if (std::adjacent_find(srt.begin(), srt.end()) != srt.end()) {
       set_last_error("interpolation points must be pairwise distinct");
@@ -319,7 +320,7 @@ int intbasis_run(Context& cx, uint64_t p, const void* E, int m, int n, int order
       cur = h_mulmod(cur, r, p);
       ok = cur == pts[t];
     }
-    static const bool off = std::getenv("FPM_NO_CHIRP") != nullptr;
+    const bool off = option(kOptNoChirp) != 0;
     if (ok && !off) geo = GeoPts{true, (uint32_t)r, (uint32_t)h_invmod(r, p)};
   }
   if (T < 1) T = 1;
@@ -387,7 +388,7 @@ int eval_points_run(Context& cx, uint64_t p, const void* P, int m, int n, int L,
       cur = h_mulmod(cur, r, p);
       ok = cur == pts[t];
     }
-    static const bool off = std::getenv("FPM_NO_CHIRP") != nullptr;
+    const bool off = option(kOptNoChirp) != 0;
     if (ok && !off)
       return eval_points_geo(cx, (uint32_t)p, (const uint32_t*)P, L, L, (long long)m * n, a_dev,
                              npts, GeoPts{true, (uint32_t)r, (uint32_t)h_invmod(r, p)},

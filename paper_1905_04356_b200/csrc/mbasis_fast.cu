@@ -982,10 +982,13 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   sa.m = m; sa.n = n; sa.T = order; sa.s = s_dev;
   sa.rec_np = rec_np; sa.rec_plist = rec_plist; sa.rec_Ct = rec_Ct;
   sa.sft_out = sft_dev; sa.fold_k = K; sa.f = f;
+#ifdef FPM_TRACE
+  // profiling build only (tools/mbasis_trace.py)
   if (std::getenv("FPM_MBASIS_TRACE")) {
     if (!g_step_trace) cudaMalloc(&g_step_trace, 64 * 8 * sizeof(unsigned long long));
     sa.trace = g_step_trace;
   }
+#endif
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     FPM_CUDA_TRY(cudaFuncSetAttribute(mbasis_steps_kernel,
@@ -1018,6 +1021,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
 
 }  // namespace fpm
 
+#ifdef FPM_TRACE
 // profiling only: per-step phase clocks of the last leaf (FPM_MBASIS_TRACE)
 extern "C" int fpm_debug_mbasis_trace(unsigned long long* host) {
   if (!fpm::g_step_trace) return 1;
@@ -1026,3 +1030,4 @@ extern "C" int fpm_debug_mbasis_trace(unsigned long long* host) {
              cudaMemcpyDeviceToHost);
   return 0;
 }
+#endif

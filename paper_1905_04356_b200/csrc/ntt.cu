@@ -383,7 +383,7 @@ int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
 }  // namespace
 
 int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStream_t st) {
-  static const bool no_persist = std::getenv("FPM_NTT_NO_PERSIST") != nullptr;
+  const bool no_persist = option(kOptNttGeneric) != 0;
   if (!no_persist && ntt_tma_fwd_ok(logn, a_in)) return launch_ntt_fwd_tma(logn, a_in, ps, st);
   if (a_in.n_entries2 > 0) {
     if (!no_persist && ntt_persist_fwd_ok(logn, a_in) && a_in.n_entries > 0)
@@ -419,7 +419,7 @@ int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStr
 
 int launch_ntt_inv(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
   if (a.n_entries <= 0) return kOk;
-  static const bool no_persist = std::getenv("FPM_NTT_NO_PERSIST") != nullptr;
+  const bool no_persist = option(kOptNttGeneric) != 0;
   if (!no_persist && ntt_tma_inv_ok(logn, a)) return launch_ntt_inv_tma(logn, a, ps, st);
   if (!no_persist && ntt_persist_inv_ok(logn, a)) return launch_ntt_inv_persist(logn, a, ps, st);
   switch (logn) {

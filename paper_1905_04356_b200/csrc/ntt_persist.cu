@@ -548,13 +548,13 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
   CUtensorMap om1{}, om2{};
   constexpr bool kTmaPm = G::TPC == 4 && !G::PAIRED;  // N = 2048, 4096 (measured: smaller N lose)
   if constexpr (kTmaPm && !FWD) {
-    static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
+    const bool off = option(kOptNttPmLsu) != 0;
     a.tma_pm = (!off && a.pm &&
                 pm_map(&om1, const_cast<uint32_t*>(a.in), a.n_entries, G::N, a.in_prime_stride,
                        ps.count, G::TPC)) ? 1 : 0;
   }
   if constexpr (kTmaPm && FWD) {
-    static const bool off = std::getenv("FPM_NTT_PM_LSU") != nullptr;
+    const bool off = option(kOptNttPmLsu) != 0;
     a.tma_pm = 0;
     if (!off && a.pm &&
         pm_map(&om1, a.out, a.n_entries, G::N, a.out_prime_stride, ps.count, G::TPC)) {
@@ -601,7 +601,7 @@ int persist_launch(const Args& a_in, const PrimeSet& ps, cudaStream_t st) {
 
 template <int LOGN, bool FWD, typename Args>
 int persist_impl(const Args& a, const PrimeSet& ps, cudaStream_t st) {
-  static const bool pm_scatter = std::getenv("FPM_PM_SCATTER") != nullptr;
+  const bool pm_scatter = option(kOptNttPmScatter) != 0;
   if (a.pm && pm_scatter && (1 << LOGN) >= 256) {
     return ps.count == 1 ? persist_launch<LOGN, true, 1, FWD>(a, ps, st)
                          : persist_launch<LOGN, false, 1, FWD>(a, ps, st);

@@ -81,7 +81,6 @@ struct TmaFwdArgs {
   int len;       // coefficients per entry (multiple of 4)
   int in_words;  // input buffer words: N/2 (upper half zero) or N
   int pl;        // eval block log: 5 (E[N/32][e][32]) or 2 (E[N/4][e][4])
-  int diag;      // FPM_NTT_DIAG bit 0: skip the output stores (timing experiments only)
 };
 
 struct TmaInvArgs {
@@ -293,7 +292,7 @@ __global__ void __launch_bounds__(TG<LOGN, G>::THREADS, 1)
           make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     tc::fence_proxy_async();
     gsync(bar, T::TPT);
-    if (leader && !(a.diag & 1)) {
+    if (leader) {
       const CUtensorMap* om = second ? &om2 : &om1;
       const int e = (int)(second ? item - a.n1 : item);
       if constexpr (PL == 5) {
@@ -467,16 +466,6 @@ int make_eval_map(CUtensorMap* m, const uint32_t* base, long long n_entries, int
   return kOk;
 }
 
-int tma_threads() {
-  static int t = -1;
-  if (t < 0) {
-    const char* s = std::getenv("FPM_NTT_TMA_THREADS");
-    t = s ? std::atoi(s) : 512;
-    if (t != 768) t = 512;
-  }
-  return t;
-}
-
 int sm_count() {
   static int sms = 0;
   if (!sms) {
@@ -532,8 +521,6 @@ int fwd_launch(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t st) {
   a.len = f.len;
   a.in_words = f.len <= T::N / 2 ? T::N / 2 : T::N;
   a.pl = f.pblk_log ? f.pblk_log : 5;
-  static const int diag = std::getenv("FPM_NTT_DIAG") ? std::atoi(std::getenv("FPM_NTT_DIAG")) : 0;
-  a.diag = diag;
   CUtensorMap m1, m2;
   FPM_TRY(make_eval_map(&m1, f.out, f.n_entries, T::N, a.pl, f.out_prime_stride, ps.count));
   if (two)
@@ -569,21 +556,18 @@ int inv_launch(const NttInvArgs& f, const PrimeSet& ps, cudaStream_t st) {
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-// variant 0: 512 threads per CTA; 1: 768 (FPM_NTT_TMA_THREADS=768);
+// variant 0: 512 threads per CTA (768 measured slower: spills);
 // 2: one group per CTA, for batches too small to give every SM two groups
 // (cfg1: latency, not throughput)
 template <int PL>
 int fwd_pl(int logn, int var, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
   switch (logn) {
     case 11:
-      return var == 2 ? fwd_launch<11, 1, PL>(a, ps, st)
-                      : var == 1 ? fwd_launch<11, 12, PL>(a, ps, st) : fwd_launch<11, 8, PL>(a, ps, st);
+      return var == 2 ? fwd_launch<11, 1, PL>(a, ps, st) : fwd_launch<11, 8, PL>(a, ps, st);
     case 12:
-      return var == 2 ? fwd_launch<12, 1, PL>(a, ps, st)
-                      : var == 1 ? fwd_launch<12, 6, PL>(a, ps, st) : fwd_launch<12, 4, PL>(a, ps, st);
+      return var == 2 ? fwd_launch<12, 1, PL>(a, ps, st) : fwd_launch<12, 4, PL>(a, ps, st);
     case 13:
-      return var == 2 ? fwd_launch<13, 1, PL>(a, ps, st)
-                      : var == 1 ? fwd_launch<13, 3, PL>(a, ps, st) : fwd_launch<13, 2, PL>(a, ps, st);
+      return var == 2 ? fwd_launch<13, 1, PL>(a, ps, st) : fwd_launch<13, 2, PL>(a, ps, st);
   }
   return kUnsupported;
 }
@@ -591,27 +575,24 @@ template <int PL>
 int inv_pl(int logn, int var, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
   switch (logn) {
     case 11:
-      return var == 2 ? inv_launch<11, 1, PL>(a, ps, st)
-                      : var == 1 ? inv_launch<11, 12, PL>(a, ps, st) : inv_launch<11, 8, PL>(a, ps, st);
+      return var == 2 ? inv_launch<11, 1, PL>(a, ps, st) : inv_launch<11, 8, PL>(a, ps, st);
     case 12:
-      return var == 2 ? inv_launch<12, 1, PL>(a, ps, st)
-                      : var == 1 ? inv_launch<12, 6, PL>(a, ps, st) : inv_launch<12, 4, PL>(a, ps, st);
+      return var == 2 ? inv_launch<12, 1, PL>(a, ps, st) : inv_launch<12, 4, PL>(a, ps, st);
     case 13:
-      return var == 2 ? inv_launch<13, 1, PL>(a, ps, st)
-                      : var == 1 ? inv_launch<13, 3, PL>(a, ps, st) : inv_launch<13, 2, PL>(a, ps, st);
+      return var == 2 ? inv_launch<13, 1, PL>(a, ps, st) : inv_launch<13, 2, PL>(a, ps, st);
   }
   return kUnsupported;
 }
 
 int small_batch(long long items, int primes) {
-  static const bool off = std::getenv("FPM_NTT_NO_SMALL") != nullptr;
+  const bool off = option(kOptNttNoSmall) != 0;
   return !off && items * primes <= 2LL * sm_count();
 }
 
 }  // namespace
 
 bool ntt_tma_fwd_ok(int logn, const NttFwdArgs& a) {
-  static const bool off = std::getenv("FPM_NTT_NO_TMA") != nullptr;
+  const bool off = option(kOptNttNoTma) != 0;
   if (off || logn < 11 || logn > 13) return false;
   if (a.fold || a.in64 || a.reduce || a.natural || a.pm) return false;
   const int pl = a.pblk_log ? a.pblk_log : 5;
@@ -628,7 +609,7 @@ bool ntt_tma_fwd_ok(int logn, const NttFwdArgs& a) {
 }
 
 bool ntt_tma_inv_ok(int logn, const NttInvArgs& a) {
-  static const bool off = std::getenv("FPM_NTT_NO_TMA") != nullptr;
+  const bool off = option(kOptNttNoTma) != 0;
   if (off || logn < 11 || logn > 13) return false;
   if (a.natural || a.pm || !a.scale || a.n_entries <= 0) return false;
   const int pl = a.pblk_log ? a.pblk_log : 5;
@@ -637,14 +618,13 @@ bool ntt_tma_inv_ok(int logn, const NttInvArgs& a) {
 }
 
 int launch_ntt_fwd_tma(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  int var = tma_threads() == 768 ? 1 : 0;
-  if (var == 1 && logn == 13 && fwd_smem<13, 3>(a.len) > kMaxSmem) var = 0;
+  int var = 0;
   if (small_batch((long long)a.n_entries + (a.n_entries2 > 0 ? a.n_entries2 : 0), ps.count)) var = 2;
   return (a.pblk_log == 2) ? fwd_pl<2>(logn, var, a, ps, st) : fwd_pl<5>(logn, var, a, ps, st);
 }
 
 int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
-  int var = tma_threads() == 768 && logn == 11 ? 1 : 0;  // 3 groups of 2^12/2^13 do not fit
+  int var = 0;
   if (small_batch(a.n_entries, ps.count)) var = 2;
   return (a.pblk_log == 2) ? inv_pl<2>(logn, var, a, ps, st) : inv_pl<5>(logn, var, a, ps, st);
 }

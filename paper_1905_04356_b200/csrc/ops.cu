@@ -5,7 +5,6 @@
 #include "ntt.cuh"
 #include "pointwise.cuh"
 #include "tc_pointwise.cuh"
-#include <cstdlib>
 
 namespace fpm {
 
@@ -106,18 +105,27 @@ bool direct_ok(uint64_t p, int logn) {
 }  // namespace
 
 int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L, int* deg) {
-  if (entries <= 0 || L <= 0) {
-    *deg = -1;
-    return kOk;
-  }
+  return matrix_degrees(cx, M, is64, entries, L, nullptr, 0, 0, deg, nullptr);
+}
+
+int matrix_degrees(Context& cx, const void* M1, int is64, long long e1, int L1, const void* M2,
+                   long long e2, int L2, int* deg1, int* deg2) {
+  const bool two = deg2 != nullptr;
+  const bool any1 = e1 > 0 && L1 > 0, any2 = two && e2 > 0 && L2 > 0;
+  *deg1 = -1;
+  if (two) *deg2 = -1;
+  if (!any1 && !any2) return kOk;
   Workspace ws(cx);
   int* d = nullptr;
-  FPM_TRY(ws.get(1, &d));
-  FPM_TRY(launch_max_len(M, is64, entries, L, d, cx.stream()));
-  int h = 0;
-  FPM_CUDA_TRY(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, cx.stream()));
+  FPM_TRY(ws.get(2, &d));
+  if (any1) FPM_TRY(launch_max_len(M1, is64, e1, L1, d, cx.stream()));
+  if (any2) FPM_TRY(launch_max_len(M2, is64, e2, L2, d + 1, cx.stream()));
+  int h[2] = {0, 0};
+  FPM_CUDA_TRY(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, cx.stream()));
+  // the one host synchronisation of the degree-dependent entry points
   FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
-  *deg = h - 1;
+  *deg1 = h[0] - 1;
+  if (two) *deg2 = h[1] - 1;
   return kOk;
 }
 
@@ -180,30 +188,16 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   FPM_TRY(ws.get(r * N * ec, &EC));
 
   const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
-  // large contractions: int8 tensor-core pointwise on point-major operands
-  // small matrices (m <= 128): grouped TMA-fed kernel, G points per UMMA tile
-  static const bool tc_off = std::getenv("FPM_DISABLE_TC") != nullptr;
-  static const bool small_off = std::getenv("FPM_DISABLE_TC_SMALL") != nullptr;
-  // point-quad TC kernel for 16 < m <= 32 (cfg2: 0.205 vs 0.225 ms on the
-  // CUDA cores); m <= 16 stays on the CUDA cores (cfg3: 35 vs 75 us)
-  static const bool pq_off = std::getenv("FPM_DISABLE_TC_PQ") != nullptr;
-  // limbs-on-M variant (tc_pq2.cu): exact and TMEM-light, but its shuffle
-  // reduce-scatter epilogue costs more than it saves on cfg2 (49.5 vs 45 us);
-  // opt-in until that epilogue is cheaper
-  static const bool pq2_on = std::getenv("FPM_ENABLE_TC_PQ2") != nullptr;
-  bool pq2 = !tc_off && pq2_on && logn <= 13 && (long long)m * k * n >= 4096;
-  for (int i = 0; i < r && pq2; ++i) pq2 = tc_pq2_applicable(m, k, n, (int)N, primes[i]);
-  bool pq = pq2;
-  if (!pq2) {
-    pq = !tc_off && !pq_off && logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
-    for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
-  }
-  // grouped / M-tiled PM-layout TC kernel (TMA, warp specialised) for m > 32;
-  // tc_pointwise.cu remains for shapes it does not take (p < 2^30)
-  bool grouped = !pq && !tc_off && !small_off && logn <= 13 && m > 32 &&
-                 (long long)m * k * n >= 4096;
+  // pointwise engine: int8 tensor cores where the contraction is a real dense
+  // product, CUDA cores otherwise (m <= 16: cfg3 35 vs 75 us on the TC path)
+  // - point-quad kernel (tc_pq.cu) for 16 < m <= 32 (cfg2: 0.205 vs 0.225 ms)
+  // - grouped / M-tiled point-major kernel (tc_grouped.cu) for m > 32
+  // - tc_pointwise.cu for shapes neither takes (p < 2^30)
+  bool pq = logn <= 13 && m > 16 && (long long)m * k * n >= 4096;
+  for (int i = 0; i < r && pq; ++i) pq = tc_pq_applicable(m, k, n, (int)N, primes[i]);
+  bool grouped = !pq && logn <= 13 && m > 32 && (long long)m * k * n >= 4096;
   for (int i = 0; i < r && grouped; ++i) grouped = tc_grouped_applicable(m, k, n, primes[i]);
-  bool use_tc = !tc_off && logn <= 13;
+  bool use_tc = logn <= 13;
   for (int i = 0; i < r && use_tc; ++i) use_tc = tc_pointwise_applicable(m, k, n, primes[i]);
   use_tc = !pq && (use_tc || grouped);
   // forward transforms (all primes in one launch: blockIdx.z = prime)
@@ -277,7 +271,6 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   if (!b_cached) FPM_TRY(to_u32(fb, eb));
   // both operands in one launch when their transforms are alike (persistent
   // grid: one tail wave instead of two)
-  static const bool no_pair = std::getenv("FPM_NTT_NO_PAIR") != nullptr;
   if (!a_cached) FPM_TRY(to_u32(fa, ea));
   if (a_cached && b_cached) {
     // both evaluations reused
@@ -287,7 +280,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   } else if (b_cached) {
     StageTimer t_(cx, "ntt_fwd_A");
     FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
-  } else if (!no_pair && fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
+  } else if (fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
              fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
     NttFwdArgs fab = fa;
     fab.in2 = fb.in; fab.in2_stride = fb.in_stride; fab.in2_prime_stride = fb.in_prime_stride;
@@ -311,10 +304,7 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
     ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
     StageTimer t_(cx, "pointwise_tc");
-    if (pq2)
-      FPM_TRY(launch_tc_pq2(ta, ps, st));
-    else
-      FPM_TRY(launch_tc_pq(ta, ps, st));
+    FPM_TRY(launch_tc_pq(ta, ps, st));
   } else if (use_tc) {
     TcArgs ta{};
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
@@ -429,9 +419,10 @@ int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef
   MiddleEntryArgs ma{};
   ma.A = A.ptr; ma.B = B.ptr; ma.out = C.ptr;
   ma.in64 = A.is64; ma.out64 = C.is64;
-  if (A.is64 != B.is64 || A.is64 != C.is64 || A.stride != A.len || B.stride != B.len ||
-      C.stride != d || C.len != d) {
-    set_last_error("entrywise middle product needs dense operands of one element width");
+  // the kernel trims every entry within its stride (a basis P1 has room for
+  // order+1 coefficients but length deg P1 + 1), so only C must be dense
+  if (A.is64 != B.is64 || A.is64 != C.is64 || C.stride != d || C.len != d) {
+    set_last_error("entrywise middle product needs operands of one element width");
     return kInvalidArgument;
   }
   ma.m = m; ma.k = k; ma.n = n; ma.la = (int)A.stride; ma.lb = (int)B.stride;

@@ -64,6 +64,10 @@ int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef
 int ceil_log2_min1(long long need);
 
 // device-side degree of a dense matrix (max trimmed length - 1), synchronous
+// deg = max entry degree (-1 for zero); synchronizes the context stream once
+// (the reference's dispatch depends on the degrees, polmat.py:477-497)
 int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L, int* deg);
+int matrix_degrees(Context& cx, const void* M1, int is64, long long e1, int L1, const void* M2,
+                   long long e2, int L2, int* deg1, int* deg2);
 
 }  // namespace fpm

@@ -458,12 +458,12 @@ int pmbasis_run(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
     // (cfg4 with the tensor-core residual update, tools/pmb_T.py: T = 32
     // 95.7 ms, 16 95.6, 12 93.7, 8 93.7)
     const int tf = mbasis_fast_max_order(m, n);
-    static const int tmax = std::getenv("FPM_PMBASIS_TMAX") ? std::atoi(std::getenv("FPM_PMBASIS_TMAX")) : 8;
+    const int tmax = (int)option(kOptPmbasisLeaf);
     const int tcap = tf < tmax ? tf : tmax;
     if (tf >= 1 && T > tcap) T = tcap;
   }
   std::vector<int64_t> s(shift, shift + m);
-  static const bool dev_off = std::getenv("FPM_PMBASIS_HOST_SYNC") != nullptr;
+  const bool dev_off = option(kOptPmbasisHostSync) != 0;
   if (!dev_off && !is64 && p < (1ull << 31) && m > 0 && order >= 1 && T >= 1 &&
       T <= mbasis_fast_max_order(m, n) && ps >= order + 1) {
     Workspace ws(cx);

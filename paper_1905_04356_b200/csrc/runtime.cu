@@ -47,6 +47,82 @@ int h_two_adicity(uint64_t p) {
   while (m && (m & 1) == 0) { m >>= 1; ++k; }
   return k;
 }
+// ---- factorisation of n < 2^64 (host): small primes by division, the
+// cofactor split by Pollard's rho with Brent's cycle search and batched gcds
+namespace {
+uint64_t gcd_u64(uint64_t a, uint64_t b) {
+  while (b) {
+    const uint64_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+uint64_t rho_split(uint64_t n) {
+  if ((n & 1) == 0) return 2;
+  for (uint64_t c = 1;; ++c) {
+    auto f = [&](uint64_t x) { return (uint64_t)(((u128)x * x + c) % n); };
+    uint64_t y = 2, x = 2, g = 1, q = 1, ys = 2;
+    const uint64_t batch = 64;
+    for (uint64_t r = 1; g == 1; r <<= 1) {
+      x = y;
+      for (uint64_t i = 0; i < r; ++i) y = f(y);
+      for (uint64_t k = 0; k < r && g == 1; k += batch) {
+        ys = y;
+        const uint64_t lim = (r - k) < batch ? (r - k) : batch;
+        for (uint64_t i = 0; i < lim; ++i) {
+          y = f(y);
+          q = h_mulmod(q, x > y ? x - y : y - x, n);
+        }
+        g = gcd_u64(q, n);
+      }
+    }
+    if (g == n) {
+      // the batch overshot: step one at a time from its start
+      do {
+        ys = f(ys);
+        g = gcd_u64(x > ys ? x - ys : ys - x, n);
+      } while (g == 1);
+    }
+    if (g != n) return g;
+  }
+}
+void factor_rec(uint64_t n, std::map<uint64_t, int>& out) {
+  if (n == 1) return;
+  if (h_is_prime(n)) {
+    ++out[n];
+    return;
+  }
+  const uint64_t d = rho_split(n);
+  factor_rec(d, out);
+  factor_rec(n / d, out);
+}
+}  // namespace
+
+std::map<uint64_t, int> h_factorize(uint64_t n) {
+  std::map<uint64_t, int> out;
+  if (n < 2) return out;
+  for (uint64_t q = 2; q < 1024 && q * q <= n; q += (q == 2 ? 1 : 2))
+    while (n % q == 0) {
+      ++out[q];
+      n /= q;
+    }
+  factor_rec(n, out);
+  return out;
+}
+
+uint64_t h_element_order(uint64_t p, uint64_t a, const std::map<uint64_t, int>& fac) {
+  // smallest divisor d of p - 1 with a^d = 1: strip each prime factor while
+  // the power stays 1
+  uint64_t ord = p - 1;
+  for (const auto& qe : fac)
+    for (int e = 0; e < qe.second; ++e) {
+      if (h_powmod(a, ord / qe.first, p) != 1) break;
+      ord /= qe.first;
+    }
+  return ord;
+}
+
 uint64_t h_ntt_root(uint64_t p) {
   const int k = h_two_adicity(p);
   uint64_t a = 2;
@@ -297,10 +373,50 @@ void Context::give_event(cudaEvent_t e) {
   ev_pool_.push_back(e);
 }
 
-bool pdl_enabled() {
-  static const bool on = std::getenv("FPM_NO_PDL") == nullptr;
-  return on;
+namespace {
+struct OptDef {
+  const char* name;
+  long long dflt;
+};
+const OptDef kOptDefs[kOptCount] = {
+    {"no_pdl", 0},      {"host_blocks", 0},   {"no_chirp", 0},     {"ntt_generic", 0},
+    {"ntt_no_tma", 0},  {"ntt_no_small", 0},  {"ntt_pm_lsu", 0},   {"ntt_pm_scatter", 0},
+    {"pmbasis_leaf", 8}, {"pmbasis_host_sync", 0},
+};
+std::atomic<long long> g_opt[kOptCount] = {};
+std::atomic<bool> g_opt_init{false};
+std::mutex g_opt_mu;
+void opt_init() {
+  if (g_opt_init.load(std::memory_order_acquire)) return;
+  std::lock_guard<std::mutex> lk(g_opt_mu);
+  if (g_opt_init.load(std::memory_order_relaxed)) return;
+  for (int i = 0; i < kOptCount; ++i) g_opt[i].store(kOptDefs[i].dflt);
+  g_opt_init.store(true, std::memory_order_release);
 }
+}  // namespace
+
+long long option(Option o) {
+  opt_init();
+  return g_opt[o].load(std::memory_order_relaxed);
+}
+
+int set_option(const char* name, long long value) {
+  opt_init();
+  if (!name) {
+    // reset every option to its default
+    for (int i = 0; i < kOptCount; ++i) g_opt[i].store(kOptDefs[i].dflt);
+    return kOk;
+  }
+  for (int i = 0; i < kOptCount; ++i)
+    if (std::strcmp(name, kOptDefs[i].name) == 0) {
+      g_opt[i].store(value);
+      return kOk;
+    }
+  set_last_error("unknown option '%s'", name);
+  return kInvalidArgument;
+}
+
+bool pdl_enabled() { return option(kOptNoPdl) == 0; }
 
 int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   const Plan* pl = nullptr;

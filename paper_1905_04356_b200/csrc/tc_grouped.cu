@@ -362,8 +362,10 @@ int launch_nb(const CUtensorMap& mA, const CUtensorMap& mB, const GArgs& a, cons
 }  // namespace
 
 bool tc_grouped_applicable(int m, int k, int n, uint32_t p) {
-  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && k >= 1 && (k % 4) == 0 && n >= 1 &&
-         (n % 4) == 0;
+  // k <= 8192: one s32 TMEM accumulator per limb diagonal takes every K
+  // chunk, and the epilogue's bound D_r < 4k*255^2 <= 2^31 needs it
+  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && k >= 1 && k <= kTcMaxK && (k % 4) == 0 &&
+         n >= 1 && (n % 4) == 0;
 }
 
 int launch_tc_grouped(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 bool tc_pointwise_applicable(int m, int k, int n, uint32_t p) {
-  return p < (1u << 31) && (k % 4) == 0 && k >= 64 && k <= 8192 && m >= 64 && n >= 32;
+  return p < (1u << 31) && (k % 4) == 0 && k >= 64 && k <= kTcMaxK && m >= 64 && n >= 32;
 }
 
 int launch_tc_pointwise(const TcArgs& a, const PrimeSet& ps, cudaStream_t st) {

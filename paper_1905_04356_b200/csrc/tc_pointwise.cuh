@@ -13,6 +13,11 @@ struct TcArgs {
   long long a_ps, b_ps, c_ps;  // per-prime strides (elements)
 };
 
+// Largest contraction the int8 kernels take: each limb-diagonal accumulator
+// sums 4k byte products (< 255^2), all K chunks into one s32 TMEM column, so
+// D_r < 4k*255^2 <= 2^31 needs k <= 8192.  Larger k runs on the CUDA cores.
+constexpr int kTcMaxK = 8192;
+
 bool tc_pointwise_applicable(int m, int k, int n, uint32_t p);
 int launch_tc_pointwise(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 
@@ -24,9 +29,5 @@ int launch_tc_grouped(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 // m <= 32 on the point-quad eval layout X[t/4][entry][t%4] (tc_pq.cu)
 bool tc_pq_applicable(int m, int k, int n, int npts, uint32_t p);
 int launch_tc_pq(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
-
-// m, n <= 32 on the point-quad layout, limbs on M (tc_pq2.cu)
-bool tc_pq2_applicable(int m, int k, int n, int npts, uint32_t p);
-int launch_tc_pq2(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 
 }  // namespace fpm

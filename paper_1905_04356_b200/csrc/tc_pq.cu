@@ -533,8 +533,9 @@ unsigned long long* trace = nullptr;  // FPM_TCPQ_DBG & 32: per-item timestamps
 }  // namespace
 
 bool tc_pq_applicable(int m, int k, int n, int npts, uint32_t p) {
-  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && m <= 32 && k >= 1 && n >= 1 &&
-         (npts % 8) == 0;
+  // k <= 8192: see tc_grouped_applicable (accumulator bound D_r < 2^31)
+  return p < (1u << 31) && p >= (1u << 30) && m >= 1 && m <= 32 && k >= 1 && k <= kTcMaxK &&
+         n >= 1 && (npts % 8) == 0;
 }
 
 int launch_tc_pq(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
@@ -547,6 +548,8 @@ int launch_tc_pq(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
   QArgs a{};
   a.C = t.C; a.m = t.m; a.k = t.k; a.n = t.n; a.npts = t.npts; a.nz = ps.count;
   a.c_ps = t.c_ps;
+#ifdef FPM_TRACE
+  // profiling build only (tools/tcpq_trace.py): per-item phase clocks
   static const int dbg = std::getenv("FPM_TCPQ_DBG") ? std::atoi(std::getenv("FPM_TCPQ_DBG")) : 0;
   a.dbg = dbg;
   if ((dbg & 32) && !trace) {
@@ -554,13 +557,16 @@ int launch_tc_pq(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
     cudaMemset(trace, 0, 64 * 8 * sizeof(unsigned long long));
   }
   a.trace = (dbg & 32) ? trace : nullptr;
+#else
+  a.dbg = 0;
+  a.trace = nullptr;
+#endif
   a.mp = t.m <= 16 ? 16 : 32;
   a.G = 128 / a.mp;
   // NB: power of two, G accumulators of 4 NB columns fit the 512 TMEM columns
   // NB <= mp/2 when FPM_TCPQ_HALF: TMEM holds two items' accumulators
-  static const bool half = std::getenv("FPM_TCPQ_HALF") != nullptr;
   int nb = 8;
-  while (nb < t.n && nb < (half ? a.mp / 2 : a.mp)) nb <<= 1;
+  while (nb < t.n && nb < a.mp) nb <<= 1;
   a.nblk = (t.n + nb - 1) / nb;
   a.ngroups = (t.npts + a.G - 1) / a.G;
   a.nch = (t.k + 31) / 32;
@@ -607,9 +613,11 @@ int launch_tc_pq(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
 }  // namespace fpm
 
 // profiling only: timestamps recorded by CTA 0 under FPM_TCPQ_DBG & 32
+#ifdef FPM_TRACE
 extern "C" int fpm_debug_tcpq_trace(unsigned long long* host) {
   if (!fpm::trace) return 1;
   cudaDeviceSynchronize();
   cudaMemcpy(host, fpm::trace, 64 * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
   return 0;
 }
+#endif

@@ -157,25 +157,3 @@ extern "C" int fpm_selftest_tc_pq(fpm_context* ctx, const uint32_t* primes, int 
   FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
   return kOk;
 }
-
-// limbs-on-M point-quad kernel for tests (same layout as fpm_selftest_tc_pq)
-extern "C" int fpm_selftest_tc_pq2(fpm_context* ctx, const uint32_t* primes, int nprimes,
-                                   const void* A, const void* B, void* C, int m, int k, int n,
-                                   int npts) {
-  using namespace fpm;
-  if (!ctx || nprimes < 1 || nprimes > 8) {
-    set_last_error("tc_pq2 selftest: bad arguments");
-    return kInvalidArgument;
-  }
-  PrimeSet ps;
-  ps.count = nprimes;
-  for (int i = 0; i < nprimes; ++i) FPM_TRY(ctx->cx->prime_const(primes[i], 5, &ps.pr[i]));
-  TcArgs a{};
-  a.A = (const uint32_t*)A; a.B = (const uint32_t*)B; a.C = (uint32_t*)C;
-  a.m = m; a.k = k; a.n = n; a.npts = npts;
-  a.a_ps = (long long)npts * m * k; a.b_ps = (long long)npts * k * n;
-  a.c_ps = (long long)npts * m * n;
-  FPM_TRY(launch_tc_pq2(a, ps, ctx->cx->stream()));
-  FPM_CUDA_TRY(cudaStreamSynchronize(ctx->cx->stream()));
-  return kOk;
-}

@@ -155,7 +155,21 @@ def intbasis_dense(E, alpha, s, p):
 
         raise LengthMismatch("one point per constant matrix")
     s_arr = (ctypes.c_int64 * max(m, 1))(*[int(x) for x in s])
-    a_arr = (ctypes.c_uint64 * max(order, 1))(*[int(x) % p for x in alpha])
+    # appint._check_points compares the integers as given (appint.py:203-205);
+    # the C ABI does the same on uint64 values, so residues that repeat among
+    # distinct integers (1 and 1 + p) are passed as distinct representatives
+    if len(set(int(x) for x in alpha)) != len(alpha):
+        from .errors import DuplicatePoints
+
+        raise DuplicatePoints("interpolation points must be pairwise distinct")
+    seen = {}
+    reps = []
+    for x in alpha:
+        r = int(x) % p
+        c = seen.get(r, 0)
+        seen[r] = c + 1
+        reps.append(r + c * p)
+    a_arr = (ctypes.c_uint64 * max(order, 1))(*reps)
     P = torch.zeros((m, m, order + 1), dtype=E.dtype, device=E.device)
     lp = ctypes.c_int(0)
     rd = (ctypes.c_int64 * max(m, 1))()

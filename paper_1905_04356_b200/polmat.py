@@ -338,36 +338,23 @@ def multiplier_apply(mult, B):
 
 
 # ---- text interchange (polmat.py:617-647) -----------------------------------
+# The reference's text format, written and parsed natively (csrc/textio.cu via
+# textio.dense_to_text / dense_from_text), byte for byte the same.
 
 def polmat_to_text(A):
-    lines = [f"{A.ctx.p} {A.m} {A.n}"]
-    for row in A.rows:
-        for e in row:
-            lines.append(" ".join(str(c) for c in e))
-    return "\n".join(lines) + "\n"
+    from . import textio
+
+    L = max(A.degree + 1, 0)
+    return textio.dense_to_text(to_dense(A, L), A.ctx.p)
 
 
 def polmat_from_text(text, ctx=None):
-    lines = text.splitlines()
-    if not lines:
-        raise ValueError("empty matrix file")
-    head = lines[0].split()
-    if len(head) != 3:
-        raise ValueError("matrix header must be 'p m n'")
-    p, m, n = (int(t) for t in head)
+    from . import textio
+
+    p, D = textio.dense_from_text(text)
     if ctx is None or ctx.p != p:
         ctx = field_new(p)
-    body = lines[1:]
-    if len(body) < m * n:
-        body = body + [""] * (m * n - len(body))
-    rows, it = [], iter(body)
-    for _ in range(m):
-        row = []
-        for _ in range(n):
-            s = next(it).strip()
-            row.append(_trim([int(t) % p for t in s.split()]) if s else [])
-        rows.append(row)
-    return PolMat(ctx, rows, ncols=n)
+    return from_dense(ctx, D, ncols=D.shape[1])
 
 
 def random_polmat(ctx, m, n, deg, rng):

@@ -11,10 +11,10 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("N,K", [(256, 128), (128, 64), (16, 32), (256, 256)])
 def test_tc_gemm_u8(N, K):
-    L = _lib.lib()
+    L = _lib.selftest_lib()
     L.fpm_selftest_tc_gemm.restype = ctypes.c_int
     L.fpm_selftest_tc_gemm.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int] * 3
-    _lib.context()
+    _lib.selftest_context()
     g = torch.Generator().manual_seed(N + K)
     A = torch.randint(0, 256, (128, K), generator=g, dtype=torch.int32)
     B = torch.randint(0, 256, (N, K), generator=g, dtype=torch.int32)
@@ -40,11 +40,11 @@ def test_tc_pointwise_exact(m, k, n):
     import numpy as np
 
     p = 2013265921
-    L = _lib.lib()
+    L = _lib.selftest_lib()
     L.fpm_selftest_tc_pointwise.restype = ctypes.c_int
     L.fpm_selftest_tc_pointwise.argtypes = [ctypes.c_void_p, ctypes.c_uint32] + \
         [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
-    h = _lib.context()
+    h = _lib.selftest_context()
     npts = 3
     rng = np.random.default_rng(m + k + n)
     A = rng.integers(0, p, size=(npts, m, k), dtype=np.uint64)
@@ -73,11 +73,11 @@ def test_tc_grouped_exact(m, k, n, npts):
     import numpy as np
 
     primes = [2013265921, 2130706433, 1107296257]
-    L = _lib.lib()
+    L = _lib.selftest_lib()
     L.fpm_selftest_tc_grouped.restype = ctypes.c_int
     L.fpm_selftest_tc_grouped.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int] + \
         [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
-    h = _lib.context()
+    h = _lib.selftest_context()
     rng = np.random.default_rng(7 * m + 3 * k + n + npts)
     A = np.stack([rng.integers(0, q, size=(npts, m, k), dtype=np.uint64) for q in primes])
     B = np.stack([rng.integers(0, q, size=(npts, k, n), dtype=np.uint64) for q in primes])
@@ -114,22 +114,20 @@ PQ_SHAPES = [(32, 32, 32, 16), (16, 16, 16, 24), (17, 5, 9, 8), (1, 1, 1, 8), (3
              (24, 100, 40, 16), (8, 4, 4, 32), (32, 33, 70, 8)]
 
 
-@pytest.mark.parametrize("kernel", ["fpm_selftest_tc_pq", "fpm_selftest_tc_pq2"])
 @pytest.mark.parametrize("m,k,n,npts", PQ_SHAPES)
-def test_tc_pq_exact(m, k, n, npts, kernel):
+def test_tc_pq_exact(m, k, n, npts):
     """Point-quad kernel: k / n tails, m not a power of two, several n-blocks,
     three primes, a point of all p-1 (largest limb sums)."""
     import numpy as np
 
     primes = [2013265921, 2130706433, 1107296257]
-    L = _lib.lib()
+    kernel = "fpm_selftest_tc_pq"
+    L = _lib.selftest_lib()
     fn = getattr(L, kernel)
     fn.restype = ctypes.c_int
     fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int] + \
         [ctypes.c_void_p] * 3 + [ctypes.c_int] * 4
-    if kernel.endswith("pq2") and n > 32:
-        pytest.skip("tc_pq2 takes n <= 32")
-    h = _lib.context()
+    h = _lib.selftest_context()
     rng = np.random.default_rng(11 * m + 5 * k + n + npts)
     A = np.stack([rng.integers(0, q, size=(npts, m, k), dtype=np.uint64) for q in primes])
     B = np.stack([rng.integers(0, q, size=(npts, k, n), dtype=np.uint64) for q in primes])

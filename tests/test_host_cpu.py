@@ -176,3 +176,123 @@ def test_caller_goldens_present():
 
     d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "callers.json")))
     assert len(d["fracrec"]) >= 10 and len(d["kernel"]) >= 6
+
+
+def test_bridge_rebinds_the_real_reference():
+    """install_into_reference on the UNMODIFIED reference package (no compute):
+    every module that bound a hot-path name at import sees the B200 entry
+    point, and uninstall restores the reference's own functions."""
+    from refpkg import import_reference
+
+    ref = import_reference()
+    if ref is None:
+        import pytest
+
+        pytest.skip("reference fpmat not present in this container")
+    import importlib
+
+    from paper_1905_04356_b200.bridge import install_into_reference, uninstall
+
+    mods = {m: importlib.import_module(f"fpmat.{m}")
+            for m in ("polmat", "appint", "kernel", "fraction", "solve")}
+    orig = {(m, a): getattr(mod, a) for m, mod in mods.items()
+            for a in ("pm_mul", "pmbasis", "_pm_middle") if hasattr(mod, a)}
+    saved = install_into_reference(ref)
+    try:
+        for (m, a), fn in orig.items():
+            assert getattr(mods[m], a) is not fn, f"fpmat.{m}.{a} not rebound"
+        assert mods["kernel"].pmbasis.__name__ == "pmbasis"
+    finally:
+        uninstall(saved)
+    for (m, a), fn in orig.items():
+        assert getattr(mods[m], a) is fn
+
+
+def test_number_theory_matches_reference():
+    """is_prime / factorize / element_order / order_at_least (native, host)
+    against the unmodified reference's functions (modring.py:25-201)."""
+    import random
+
+    from refpkg import import_reference
+
+    from paper_1905_04356_b200 import modring as M
+
+    ref = import_reference()
+    if ref is None:
+        import pytest
+
+        pytest.skip("reference fpmat not present in this container")
+    import fpmat.modring as R
+
+    rng = random.Random(7)
+    nums = [0, 1, 2, 3, 4, 97, 561, 2013265921, 2013265920, (1 << 61) - 1, (1 << 62) - 57,
+            1152921504606846883, 3 * 5 * 7 * 11 * 13 * 17 * 19 * 23 * 29 * 31 * 37,
+            1000003 * 1000033, 4294967291 * 4294967279] + [rng.randrange(1, 1 << 62)
+                                                            for _ in range(40)]
+    for n in nums:
+        assert M.is_prime(n) == R.is_prime(n), n
+        if 1 <= n < (1 << 64):
+            assert M.factorize(n) == R.factorize(n), n
+    for p in [3, 5, 97, 65537, 786433, 2013265921, 1152921504606846883]:
+        a, b = M.field_new(p), R.field_new(p)
+        assert (a.two_adicity, a.ntt_root) == (b.two_adicity, b.ntt_root)
+        for x in [1, 2, 3, p - 1, 12345 % p or 1]:
+            assert a.element_order(x) == b.element_order(x), (p, x)
+        for n in [1, 2, 3, 4095, (p - 1) // 2, p - 1]:
+            if n <= p - 1:
+                assert M.order_at_least(a, n) == R.order_at_least(b, n), (p, n)
+        import pytest
+
+        from paper_1905_04356_b200.errors import NoSuchElement
+
+        with pytest.raises(NoSuchElement):
+            M.order_at_least(a, p)
+
+
+def test_forms_match_reference_on_random_matrices():
+    """forms.* (vectorised on the degree matrix) against the reference's
+    forms.py on random sparse matrices, zero rows and large shifts."""
+    import random
+
+    from refpkg import import_reference
+
+    from paper_1905_04356_b200 import forms, polmat
+
+    ref = import_reference()
+    if ref is None:
+        import pytest
+
+        pytest.skip("reference fpmat not present in this container")
+    import fpmat.forms as RF
+    import fpmat.polmat as RP
+    from fpmat.modring import field_new as rfield
+
+    rng = random.Random(11)
+    for trial in range(60):
+        p = rng.choice([97, 2013265921])
+        m = rng.randrange(1, 6)
+        n = m if trial % 2 == 0 else rng.randrange(1, 6)
+        rows = []
+        for i in range(m):
+            row = []
+            for j in range(n):
+                d = rng.randrange(-1, 5)
+                e = [rng.randrange(p) for _ in range(d + 1)]
+                if e:
+                    e[-1] = rng.randrange(1, p) if rng.random() < 0.7 else 1
+                row.append(e)
+            if rng.random() < 0.15:
+                row = [[] for _ in range(n)]
+            rows.append(row)
+        s = [rng.randrange(-4, 5) for _ in range(n)]
+        if trial % 7 == 0:
+            s = [x + (1 << 70) for x in s]
+        A = polmat.PolMat(polmat.field_new(p), rows, ncols=n)
+        B = RP.PolMat(rfield(p), rows, ncols=n)
+        assert forms.rdeg(A, s) == RF.rdeg(B, s)
+        assert forms.pivot_profile(A, s) == RF.pivot_profile(B, s)
+        assert forms.leading_matrix(A, s) == RF.leading_matrix(B, s)
+        if m == n:
+            assert forms.is_owp(A, s) == RF.is_owp(B, s)
+            assert forms.is_popov(A, s) == RF.is_popov(B, s)
+            assert forms.is_reduced(A, s) == RF.is_reduced(B, s)
