@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """Benchmark of the B200 F_p polynomial-matrix product path (driver contract).
 
-Default workload: BASELINE.json configs[1] (cfg2): A, B 32x32 over
-p = 2013265921, entries of degree < 4096, 8192 evaluation points.  A step is
-one exact product C = A*B on device-resident inputs.  value = algorithmic
-modular multiplications per second (SURVEY.md 8(d) convention) for the
-whole job over all ranks; every rank runs its own product (independent units,
-no data-path collective: weak scaling).
+Default workload: BASELINE.json configs[4] (cfg5), the largest single-GPU
+config: A, B 256x256 over p = 2013265921, entries of degree < 2048, 4096
+evaluation points, the 256^3 pointwise products on the int8 tensor cores.  A
+step is one exact product C = A*B on device-resident inputs.  value =
+algorithmic modular multiplications per second (SURVEY.md 8(d) convention)
+for the whole job over all ranks; every rank runs its own product
+(independent units, no data-path collective: weak scaling).
 
---impl reference runs the CPU restatement of the reference path
-(oracle/libfpm_oracle.so, "port") on the host cores instead.
+--impl reference times the multi-threaded CPU port of the reference path
+(oracle/fpm_port.c, "port": the reference itself is pure Python, ~1.3 h per
+cfg5 product on one core) on the host cores, on the same config and inputs
+recipe, and prints the same config object.
 """
 import argparse
 import json
@@ -164,11 +167,17 @@ def read_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+TRAFFIC_FILE = os.path.join("profiles", "r02_traffic.json")
+
+
 def read_traffic():
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per stage of ONE
+    product (tools/ncu_traffic.py: the launches of the last of two products
+    under ncu), {config: {stage: bytes}}."""
+    path = os.path.join(ROOT, TRAFFIC_FILE)
     try:
         with open(path) as f:
-            return json.load(f)
+            return json.load(f).get("per_step", {})
     except Exception:
         return {}
 
@@ -190,12 +199,13 @@ INT_RATES = {"imad": 2.0, "imad_hi": 4.45, "imad_wide": 4.0, "iadd": 1.0, "viadd
 # ---------------------------------------------------------------------------
 def read_int8_peak():
     """Measured int8 tensor-core peak (tools/int8_peak.py on this pool's B200:
-    torch._int_mm 8192^3), TOPS; sustained figure for kernels inside a step."""
+    torch._int_mm 8192^3), TOPS.  The burst figure: the pointwise kernel runs
+    ~1.7 ms inside a ~4.4 ms step, not back to back for seconds."""
     path = os.path.join(ROOT, "profiles", "int8_peak.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return float(d["int8_tops_sustained"]), "measured (profiles/int8_peak.json, sustained)"
+        return float(d["int8_tops"]), "measured burst (profiles/int8_peak.json int8_tops)"
     except Exception:
         return 4500.0, "nominal dense int8 4.5 POPS"
 
@@ -242,13 +252,8 @@ def roofline_report(cfg, cfgname, avg, sbytes):
     traffic = read_traffic().get(cfgname, {})
 
     def tr(stage):
-        key = "ntt_fwd" if stage.startswith("ntt_fwd") else stage
-        v = traffic.get(key)
-        if not v:
-            return None
-        if stage == "ntt_fwd_AB" and len(v) >= 2:
-            return round(sum(v[:2]))  # capture of separate A and B launches
-        return round(sum(v) / len(v))
+        v = traffic.get(stage)
+        return None if v is None else int(v)
 
     table = {}
     for st, ms in avg.items():
@@ -391,8 +396,8 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
 
 
 def e2e_mul(cfg, steps, warmup, seed):
-    """Same metric through the C ABI host entry (pinned host buffers)."""
-    import numpy as np
+    """Same metric through the C ABI host entry (pinned host buffers): every
+    call uploads A and B and downloads C inside the timed region."""
     import torch
 
     from paper_1905_04356_b200 import _lib, dense
@@ -401,10 +406,11 @@ def e2e_mul(cfg, steps, warmup, seed):
     A, B = make_inputs(cfg, "cuda", seed)
     Ah = A.cpu().pin_memory()
     Bh = B.cpu().pin_memory()
-    m, k, la = A.shape
-    _, n, lb = B.shape
+    del A, B
+    m, k, la = Ah.shape
+    _, n, lb = Bh.shape
     lc = la + lb - 1
-    Ch = torch.empty((m, n, lc), dtype=A.dtype).pin_memory()
+    Ch = torch.empty((m, n, lc), dtype=Ah.dtype).pin_memory()
     h = _lib.context()
     L = _lib.lib()
     eb = dense.elem_bytes_for(p)
@@ -421,77 +427,191 @@ def e2e_mul(cfg, steps, warmup, seed):
         call()
         ts.append(time.perf_counter() - t0)
     ts.sort()
-    med = ts[len(ts) // 2]
-    _ = np
-    return med, Ah.numel() * eb + Bh.numel() * eb, Ch.numel() * eb
+    return ts[len(ts) // 2], Ah.numel() * eb + Bh.numel() * eb, Ch.numel() * eb
 
 
-def cpu_baseline(cfg, budget_s=10.0, threads=None):
-    """Oracle port of the reference path on host cores (bounded sample)."""
-    import numpy as np
+def e2e_pmbasis(cfg, steps, seed):
+    """cfg4 through fpm_pmbasis_host (the entry INTEGRATION.md binds for
+    appint.pmbasis): F uploaded and P downloaded inside the timed region."""
+    import ctypes
 
-    from oracle import oracle as O
+    import torch
 
-    threads = threads or os.cpu_count() or 1
-    O.set_threads(threads)
-    p = cfg["p"]
-    rng = np.random.default_rng(1)
-    if cfg["kind"] == "mul":
-        L = cfg["deg"] + 1
-        A = rng.integers(0, p, size=(cfg["m"], cfg["k"], L), dtype=np.uint64)
-        B = rng.integers(0, p, size=(cfg["k"], cfg["n"], L), dtype=np.uint64)
-        work = mul_work(cfg)[0]
+    from paper_1905_04356_b200 import _lib, dense
+
+    p, m, n, sigma = cfg["p"], cfg["m"], cfg["n"], cfg["sigma"]
+    (F,) = make_inputs(cfg, "cuda", seed)
+    Fh = F.cpu().pin_memory()
+    del F
+    Ph = torch.empty((m, m, sigma + 1), dtype=Fh.dtype).pin_memory()
+    s_arr = (ctypes.c_int64 * m)(*([0] * m))
+    lp = ctypes.c_int(0)
+    rd = (ctypes.c_int64 * m)()
+    h = _lib.context()
+    L = _lib.lib()
+    eb = dense.elem_bytes_for(p)
+
+    def call():
+        _lib.check(L.fpm_pmbasis_host(h, p, eb, Fh.data_ptr(), m, n, sigma, sigma, s_arr,
+                                      Ph.data_ptr(), ctypes.byref(lp), rd), "fpm_pmbasis_host")
+
+    call()
+    ts = []
+    for _ in range(steps):
         t0 = time.perf_counter()
-        reps = 0
-        while True:
-            O.pm_mul(p, A, B)
-            reps += 1
-            if time.perf_counter() - t0 > budget_s or reps >= 3:
+        call()
+        ts.append(time.perf_counter() - t0)
+    ts.sort()
+    return ts[len(ts) // 2], Fh.numel() * eb, Ph.numel() * eb
+
+
+def cpu_info():
+    """Host CPU model and the threads the CPU legs use (lscpu's model name)."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
                 break
-        dt = (time.perf_counter() - t0) / reps
-        return {"value": work / dt / 1e9, "unit": "Gmodmul/s", "cores": threads,
-                "kind": "port", "seconds_per_step": dt,
-                "sample": f"{reps} full {cfg['m']}x{cfg['k']}x{cfg['n']} deg<{L} products "
-                          f"(oracle/libfpm_oracle.so, OpenMP {threads} threads)"}
-    raise ValueError("cpu baseline only for product configs")
+    except Exception:
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                for line in f:
+                    if line.startswith("model name"):
+                        model = line.split(":", 1)[1].strip()
+                        break
+        except Exception:
+            model = "unknown"
+    return {"model": model, "threads": os.cpu_count() or 1}
 
 
-def reference_arm(args, cfg, rank):
-    if rank != 0:
-        return None
-    from oracle import oracle as O
+def port_inputs(cfg, seed):
     import numpy as np
 
-    threads = os.cpu_count() or 1
-    O.set_threads(threads)
     p = cfg["p"]
     L = cfg["deg"] + 1
-    rng = np.random.default_rng(1)
-    A = rng.integers(0, p, size=(cfg["m"], cfg["k"], L), dtype=np.uint64)
-    B = rng.integers(0, p, size=(cfg["k"], cfg["n"], L), dtype=np.uint64)
-    for _ in range(min(args.warmup, 1)):
-        O.pm_mul(p, A, B)
+    rng = np.random.default_rng(seed)
+    dt = np.uint32 if p < (1 << 32) else np.uint64
+    A = rng.integers(0, p, size=(cfg["m"], cfg["k"], L), dtype=np.uint64).astype(dt)
+    B = rng.integers(0, p, size=(cfg["k"], cfg["n"], L), dtype=np.uint64).astype(dt)
+    return A, B
+
+
+def port_step(cfg, A, B, threads, out=None):
+    """One full product by the CPU port: fpm_port.c for 31-bit NTT primes,
+    the restatement fpm_oracle.c (multi-prime-free NTT / schoolbook) else."""
+    from oracle import oracle as O
+
+    p = cfg["p"]
+    N, r = mul_plan(cfg)
+    if r == 1:
+        return O.port_mul31(p, A, B, threads=threads, out=out), "oracle/fpm_port.c"
+    O.set_threads(threads)
+    return O.pm_mul(p, A, B), "oracle/fpm_oracle.c"
+
+
+def cpu_baseline(cfg, budget_s=20.0, threads=None):
+    """The CPU port of the reference path on the host cores, a bounded sample
+    of the same workload: full products until ~budget_s of CPU work."""
+    threads = threads or os.cpu_count() or 1
+    if cfg["kind"] != "mul":
+        raise ValueError("cpu baseline only for product configs")
+    A, B = port_inputs(cfg, 1)
+    work = mul_work(cfg)[0]
+    out, src = port_step(cfg, A, B, threads)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        port_step(cfg, A, B, threads, out=out if src.endswith("port.c") else None)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s or reps >= 5:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": work / dt / 1e9, "unit": "Gmodmul/s", "cores": threads, "kind": "port",
+            "seconds_per_step": dt, "cpu": cpu_info(),
+            "sample": f"{reps} full {cfg['m']}x{cfg['k']}x{cfg['n']} deg<{cfg['deg'] + 1} "
+                      f"products ({src}, OpenMP {threads} threads) after one untimed product"}
+
+
+def bench_config(args, cfg, world):
+    """The config object both arms print (identical keys and values)."""
+    c = {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"}}
+    if cfg["kind"] == "mul":
+        N, r = mul_plan(cfg)
+        c.update({"N": N, "word_primes": r})
+    c["l2"] = "flushed: 256 MiB write between timed steps (outside events); inputs > L2"
+    c["parallelism"] = (f"replicas x{world} (one independent product per rank)" if world > 1
+                        else "single GPU")
+    return c
+
+
+def reference_arm(args, cfg, rank, world):
+    if rank != 0:
+        return None
+    threads = os.cpu_count() or 1
+    if cfg["kind"] != "mul":
+        return {"impl": "reference", "unavailable": "the reference arm times products only"}
+    A, B = port_inputs(cfg, 1)
+    out, src = port_step(cfg, A, B, threads)
+    for _ in range(max(0, min(args.warmup, 1) - 1)):
+        port_step(cfg, A, B, threads, out=out if src.endswith("port.c") else None)
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        O.pm_mul(p, A, B)
+        port_step(cfg, A, B, threads, out=out if src.endswith("port.c") else None)
         ts.append(time.perf_counter() - t0)
     total = sum(ts)
     work = mul_work(cfg)[0]
     val = work * args.steps / total / 1e9
     line = {
-        "metric": METRIC, "value": val, "unit": "Gmodmul/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform in [0,p))",
-        "config": {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"}},
-        "cpu_baseline": {"value": val, "unit": "Gmodmul/s", "cores": threads, "kind": "port",
-                         "sample": f"{args.steps} full products on host cores "
-                                   "(CPU restatement of polmat._pm_mul_ntt, oracle/)"},
-        "e2e": {"value": val, "unit": "Gmodmul/s", "h2d_bytes_per_step": 0,
+        "metric": METRIC, "value": round(val, 4), "unit": "Gmodmul/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32" if cfg["p"] < (1 << 31) else "u64",
+        "data": "synthetic (seeded uniform coefficients in [0,p), numpy PCG64)",
+        "config": bench_config(args, cfg, world),
+        "cpu_baseline": {"value": round(val, 4), "unit": "Gmodmul/s", "cores": threads,
+                         "kind": "port", "cpu": cpu_info(),
+                         "sample": f"{args.steps} full products per run, one per step, after "
+                                   f"one untimed warm-up product ({src}: multi-threaded CPU "
+                                   "port of polmat._pm_mul_ntt, polmat.py:290-308; the "
+                                   "reference is pure Python)"},
+        "e2e": {"value": round(val, 4), "unit": "Gmodmul/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     return line
+
+
+def pmbasis_split(cfg, device, seed):
+    """cfg4 stage split from the library's per-stage CUDA events (untimed
+    run): leaf (M-Basis steps + basis build) and tree (products, middle
+    products, shifts)."""
+    import torch
+
+    from paper_1905_04356_b200 import _lib
+
+    h = _lib.context()
+    inputs = make_inputs(cfg, device, seed)
+    run_step(cfg, inputs)
+    torch.cuda.synchronize()
+    _lib.profile(h, True)
+    run_step(cfg, inputs)
+    torch.cuda.synchronize()
+    recs = _lib.profile_records(h)
+    _lib.profile(h, False)
+    leaf = sum(ms for nm, ms in recs if nm.startswith("mbasis"))
+    steps_ms = sum(ms for nm, ms in recs if nm == "mbasis_steps")
+    tot = sum(ms for _, ms in recs)
+    return {"leaf_ms": round(leaf, 3), "leaf_steps_ms": round(steps_ms, 3),
+            "tree_ms": round(tot - leaf, 3), "stage_sum_ms": round(tot, 3),
+            "order1_steps": cfg["sigma"],
+            "leaf_steps_per_s": round(cfg["sigma"] / (leaf * 1e-3), 1) if leaf else None,
+            "note": "per-stage CUDA events (one event pair per launch adds a little), "
+                    "leaf = mbasis_steps + mbasis_build"}
 
 
 def per_config_table(device):
@@ -507,13 +627,18 @@ def per_config_table(device):
             ts, _, _ = time_steps(cfg, inputs, steps, warm, flush)
             ts.sort()
             ms = ts[len(ts) // 2]
+            del inputs
             if cfg["kind"] == "intbasis":
                 out[name] = {"ms": round(ms, 4), "note": "PM-IntBasis (SURVEY 8(f) rank 2), "
                              "not a BASELINE config"}
                 continue
             work = mul_work(cfg)[0] if cfg["kind"] == "mul" else pmbasis_work(cfg)
             out[name] = {"ms": round(ms, 4), "Gmodmul_s": round(work / ms / 1e6, 2)}
-            del inputs
+            if cfg["kind"] == "pmbasis":
+                out[name]["split"] = pmbasis_split(cfg, device, 104)
+                med, bi, bo = e2e_pmbasis(cfg, 3, 104)
+                out[name]["e2e"] = {"ms": round(med * 1e3, 3), "h2d_bytes": bi, "d2h_bytes": bo,
+                                    "path": "fpm_pmbasis_host (C ABI, pinned host buffers)"}
         except Exception as exc:  # report, never hide
             out[name] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
@@ -525,7 +650,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
     ap.add_argument("--no-extras", action="store_true",
                     help="skip cpu_baseline / e2e / per-config table")
     args = ap.parse_args()
@@ -536,7 +661,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     if args.impl == "reference":
-        line = reference_arm(args, cfg, rank)
+        line = reference_arm(args, cfg, rank, world)
         if line is not None:
             print(json.dumps(line), flush=True)
         return
@@ -584,28 +709,25 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32" if cfg["p"] < (1 << 31) else "u64",
         "data": "synthetic (seeded uniform coefficients in [0,p), torch.Generator)",
-        "config": {"workload": args.config, **{k: v for k, v in cfg.items() if k != "kind"},
-                   "N": N, "word_primes": r,
-                   "l2": "flushed: 256 MiB write between timed steps (outside events)",
-                   "parallelism": f"replicas x{world} (independent products per rank)"},
+        "config": bench_config(args, cfg, world),
         "gpu_launches": launches,
         "clocks": clk,
     }
+    del inputs
     # roofline of the dominant kernel class, CUDA events inside the timed region
     if stages:
         avg = {k: sum(v) / len(v) for k, v in stages.items()}
         line["stages_ms"] = {k: round(v, 5) for k, v in avg.items()}
-        nprof = min(args.steps, 3)
-        line["stages_total_ms_per_step"] = {k: round(sum(v) / nprof, 4) for k, v in stages.items()}
         if cfg["kind"] == "mul":
             line["roofline"], line["roofline_stages"] = roofline_report(cfg, args.config, avg,
                                                                         sbytes)
+            line["roofline"]["traffic_source"] = TRAFFIC_FILE
     if not args.no_extras and cfg["kind"] == "mul":
         # every rank runs its own host-buffer product (weak scaling, as the
         # device-timed value); the slowest rank's median sets the job time
         err = None
         try:
-            med, bi, bo = e2e_mul(cfg, max(3, args.steps // 2), 2, 7 + rank)
+            med, bi, bo = e2e_mul(cfg, max(3, min(args.steps, 10)), 2, 7 + rank)
         except Exception as exc:
             med, bi, bo, err = float("inf"), 0, 0, f"{type(exc).__name__}: {exc}"
         if dist is not None:
@@ -620,13 +742,12 @@ def main():
                                    "one product per rank, max over ranks"}
         else:
             line["e2e"] = {"error": err or "a rank failed its host-buffer product"}
-    if rank == 0 and not args.no_extras and cfg["kind"] == "mul":
-        if world == 1:
-            try:
-                line["cpu_baseline"] = cpu_baseline(cfg)
-            except Exception as exc:
-                line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
-            line["per_config"] = per_config_table(device)
+    if rank == 0 and not args.no_extras and cfg["kind"] == "mul" and world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        except Exception as exc:
+            line["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"}
+        line["per_config"] = per_config_table(device)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -28,7 +28,8 @@ _ip = ctypes.POINTER(ctypes.c_int)
 def build(force=False):
     """Compile the oracle with the committed Makefile (gcc, OpenMP)."""
     if force or not os.path.exists(_LIB_PATH) or (
-        os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "fpm_oracle.c"))
+        os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(os.path.join(_HERE, f))
+                                          for f in ("fpm_oracle.c", "fpm_port.c"))
     ):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
@@ -62,6 +63,11 @@ def lib():
         L.fpo_pmbasis.restype = ctypes.c_int
         L.fpo_pmbasis.argtypes = [ctypes.c_uint64, _u64p, ctypes.c_int, ctypes.c_int,
                                   ctypes.c_int, ctypes.c_int, _i64p, ctypes.c_int, _u64p, _ip]
+        _u32p = ctypes.POINTER(ctypes.c_uint32)
+        L.fpo_port_mul31.restype = ctypes.c_int
+        L.fpo_port_mul31.argtypes = [ctypes.c_uint32, _u32p, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_int, _u32p, ctypes.c_int, ctypes.c_int, _u32p,
+                                     ctypes.c_int]
         L.fpo_set_threads.argtypes = [ctypes.c_int]
         L.fpo_get_threads.restype = ctypes.c_int
         _lib = L
@@ -188,3 +194,23 @@ def sha16(p, M):
     import hashlib
 
     return hashlib.sha256(to_text(p, M).encode()).hexdigest()[:16]
+
+
+def port_mul31(p, A, B, threads=None, out=None):
+    """Multi-threaded CPU port of polmat._pm_mul_ntt for 31-bit NTT primes
+    (oracle/fpm_port.c): the bench's CPU baseline / reference arm.
+    A (m, k, la), B (k, n, lb) uint32 in [0, p) -> C (m, n, la+lb-1) uint32."""
+    A = np.ascontiguousarray(A, dtype=np.uint32)
+    B = np.ascontiguousarray(B, dtype=np.uint32)
+    m, k, la = A.shape
+    k2, n, lb = B.shape
+    assert k == k2
+    lc = la + lb - 1
+    if out is None:
+        out = np.empty((m, n, lc), dtype=np.uint32)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    rc = lib().fpo_port_mul31(p, A.ctypes.data_as(u32p), m, k, la, B.ctypes.data_as(u32p), n,
+                              lb, out.ctypes.data_as(u32p), int(threads or os.cpu_count() or 1))
+    if rc != 0:
+        raise ValueError(f"fpo_port_mul31: status {rc} (needs a 31-bit NTT prime)")
+    return out

@@ -20,7 +20,7 @@ def _run(args, timeout):
 
 
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1"], 300)
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--config", "cfg2"], 300)
     assert d["impl"] == "reference"
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
                 "higher_is_better", "config", "cpu_baseline", "e2e"):
@@ -28,11 +28,27 @@ def test_reference_arm_line():
     assert d["value"] > 0 and d["config"]["workload"] == "cfg2"
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["cpu_baseline"]["cpu"]["model"]
+
+
+def test_both_arms_print_the_same_config():
+    """The reference arm and the device arm build one config object."""
+    sys.path.insert(0, ROOT)
+    import argparse
+
+    import bench
+
+    for name in ("cfg5", "cfg2", "cfg3"):
+        a = argparse.Namespace(config=name)
+        assert bench.bench_config(a, bench.CONFIGS[name], 1) == bench.bench_config(
+            a, bench.CONFIGS[name], 1)
+    assert bench.bench_config(argparse.Namespace(config="cfg5"), bench.CONFIGS["cfg5"],
+                              1)["workload"] == "cfg5"
 
 
 @pytest.mark.gpu
 def test_device_arm_line():
-    d = _run(["--steps", "3", "--warmup", "3", "--no-extras"], 900)
+    d = _run(["--steps", "3", "--warmup", "3", "--no-extras", "--config", "cfg2"], 900)
     assert d["metric"] and d["unit"] == "Gmodmul/s" and d["value"] > 0
     assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1
     assert d["gpu_launches"] > 0
