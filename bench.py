@@ -608,10 +608,12 @@ def pmbasis_split(cfg, device, seed):
     tot = sum(ms for _, ms in recs)
     return {"leaf_ms": round(leaf, 3), "leaf_steps_ms": round(steps_ms, 3),
             "tree_ms": round(tot - leaf, 3), "stage_sum_ms": round(tot, 3),
+            "leaf_share": round(leaf / tot, 4) if tot else None,
             "order1_steps": cfg["sigma"],
             "leaf_steps_per_s": round(cfg["sigma"] / (leaf * 1e-3), 1) if leaf else None,
-            "note": "per-stage CUDA events (one event pair per launch adds a little), "
-                    "leaf = mbasis_steps + mbasis_build"}
+            "note": "per-stage CUDA events around every launch (serialises the PDL overlap, "
+                    "so the stage sum exceeds the end-to-end time); leaf = mbasis_steps + "
+                    "mbasis_build, tree = every product / middle product / shift stage"}
 
 
 def per_config_table(device):

@@ -91,13 +91,14 @@ int fpm_order_at_least(uint64_t p, uint64_t n, uint64_t* a);
 /* ---- NTT (modring.ntt_forward / ntt_inverse, modring.py:272-286) --------
  * batch transforms of length 2^log_len, natural order in and out:
  * forward out[j] = F(w^j) with the reference root w (modring.py:233);
- * inverse applies w^-1 and scales by N^-1.  dev buffers, batch*N uint32.
- * Requires p < 2^31, 5 <= log_len <= min(15, two_adicity(p)). */
+ * inverse applies w^-1 and scales by N^-1.  dev buffers, batch*N elements.
+ * Any 0 <= log_len <= two_adicity(p) (modring.py:220-224, FPM_ERR_OUT_OF_RANGE
+ * beyond): single-CTA kernels up to 2^15, multi-pass transforms over HBM
+ * above (2^16 .. 2^27 for p = 2013265921).
+ * fpm_ntt_u32: 2 < p < 2^31.  fpm_ntt_u64: any prime 2 < p < 2^62 (31-bit
+ * primes take the u32 kernels, larger ones a radix-2 Montgomery transform). */
 int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch,
                 const uint32_t* in_dev, uint32_t* out_dev, int inverse);
-
-/* same contract for any prime 2 < p < 2^62 and any 0 <= log_len <=
- * two_adicity(p), uint64 elements (direct DFT outside the fast kernel). */
 int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch,
                 const uint64_t* in_dev, uint64_t* out_dev, int inverse);
 

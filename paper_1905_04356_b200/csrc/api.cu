@@ -54,6 +54,66 @@ int bind_device(fpm_context* ctx) {
   return kOk;
 }
 
+__global__ void widen_copy_kernel(const uint32_t* in, uint64_t* out, long long n) {
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+__global__ void narrow_copy_kernel(const uint64_t* in, uint32_t* out, long long n) {
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)in[i];
+}
+unsigned copy_grid(long long n) {
+  long long b = (n + 255) / 256;
+  return (unsigned)(b < 1 ? 1 : b > 148 * 16 ? 148 * 16 : b);
+}
+int copy_widen(const uint32_t* in, uint64_t* out, long long n, cudaStream_t st) {
+  FPM_CUDA_TRY(launch_pdl(widen_copy_kernel, dim3(copy_grid(n)), dim3(256), 0, st, in, out, n));
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+int copy_narrow(const uint64_t* in, uint32_t* out, long long n, cudaStream_t st) {
+  FPM_CUDA_TRY(launch_pdl(narrow_copy_kernel, dim3(copy_grid(n)), dim3(256), 0, st, in, out, n));
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+// modring.ntt_forward / ntt_inverse for any prime (u64 generic transform):
+// split twiddle tables built on the host per call (API path, not hot)
+int ntt64(Context& cx, uint64_t p, int log_len, int batch, const uint64_t* in, uint64_t* out,
+          int inverse) {
+  const int k = h_two_adicity(p);
+  const uint64_t N = 1ull << log_len;
+  uint64_t omega = h_powmod(h_ntt_root(p), 1ull << (k - log_len), p);
+  uint64_t scale = 1;
+  if (inverse) {
+    omega = h_invmod(omega, p);
+    scale = h_invmod(N % p, p);
+  }
+  const int h = (log_len + 1) / 2;
+  const size_t nlo = (size_t)1 << h, nhi = (size_t)((N >> h) > 0 ? (N >> h) : 1);
+  std::vector<uint64_t> lo(nlo), hi(nhi);
+  uint64_t w = 1;
+  for (size_t i = 0; i < nlo; ++i, w = h_mulmod(w, omega, p)) lo[i] = w;
+  const uint64_t step = h_powmod(omega, nlo, p);
+  w = 1;
+  for (size_t i = 0; i < nhi; ++i, w = h_mulmod(w, step, p)) hi[i] = w;
+  Workspace ws(cx);
+  uint64_t *dlo, *dhi;
+  FPM_TRY(ws.get(nlo, &dlo));
+  FPM_TRY(ws.get(nhi, &dhi));
+  FPM_CUDA_TRY(cudaMemcpyAsync(dlo, lo.data(), nlo * 8, cudaMemcpyHostToDevice, cx.stream()));
+  FPM_CUDA_TRY(cudaMemcpyAsync(dhi, hi.data(), nhi * 8, cudaMemcpyHostToDevice, cx.stream()));
+  FPM_TRY(launch_ntt64_generic(p, omega, log_len, batch, in, out, scale, dlo, dhi, h,
+                               cx.stream()));
+  // the host tables must outlive the asynchronous copies
+  FPM_CUDA_TRY(cudaStreamSynchronize(cx.stream()));
+  return kOk;
+}
+
 }  // namespace
 
 extern "C" {
@@ -172,27 +232,50 @@ int fpm_ntt_u32(fpm_context* ctx, uint32_t p, int log_len, int batch, const uint
     set_last_error("fpm_ntt_u32 needs 2 < p < 2^31");
     return kOutOfRange;
   }
-  if (log_len > h_two_adicity(p)) {
+  if (log_len < 0 || log_len > h_two_adicity(p)) {
     set_last_error("p=%u supports transforms up to length 2^%d", p, h_two_adicity(p));
     return kOutOfRange;
   }
-  if (log_len < kMinLogN || log_len > kMaxLogN) {
-    set_last_error("fpm_ntt_u32 supports 2^%d..2^%d", kMinLogN, kMaxLogN);
-    return kUnsupported;
-  }
+  if (batch <= 0) return kOk;
   Context& cx = *ctx->cx;
+  if (log_len < kMinLogN) {
+    // tiny lengths: the generic u64 transform on widened copies
+    Workspace ws(cx);
+    const size_t n = (size_t)batch << log_len;
+    uint64_t *a, *b;
+    FPM_TRY(ws.get(n, &a));
+    FPM_TRY(ws.get(n, &b));
+    FPM_TRY(copy_widen(in, a, n, cx.stream()));
+    FPM_TRY(ntt64(cx, p, log_len, batch, a, b, inverse));
+    return copy_narrow(b, out, n, cx.stream());
+  }
   PrimeSet ps;
   ps.count = 1;
   FPM_TRY(cx.prime_const(p, log_len, &ps.pr[0]));
+  const long long N = 1LL << log_len;
   if (!inverse) {
     NttFwdArgs a{};
-    a.in = in; a.in64 = 0; a.in_stride = 1LL << log_len; a.len = 1 << log_len;
+    a.in = in; a.in64 = 0; a.in_stride = N; a.len = (int)N;
     a.reduce = 0; a.fold = 0; a.natural = 1; a.n_entries = batch; a.out = out;
+    a.out_prime_stride = N * batch;
+    if (ntt_big_ok(log_len)) {
+      Workspace ws(cx);
+      uint32_t* scratch;
+      FPM_TRY(ws.get((size_t)batch * N, &scratch));
+      return launch_ntt_fwd_big(cx, log_len, a, ps, scratch, cx.stream());
+    }
     return launch_ntt_fwd(log_len, a, ps, cx.stream());
   }
   NttInvArgs a{};
   a.in = in; a.natural = 1; a.n_entries = batch; a.out = out;
-  a.out_stride = 1LL << log_len; a.out_len = 1 << log_len; a.off = 0; a.scale = 1;
+  a.in_prime_stride = N * batch;
+  a.out_stride = N; a.out_len = (int)N; a.off = 0; a.scale = 1;
+  if (ntt_big_ok(log_len)) {
+    Workspace ws(cx);
+    uint32_t* scratch;
+    FPM_TRY(ws.get((size_t)batch * N, &scratch));
+    return launch_ntt_inv_big(cx, log_len, a, ps, scratch, cx.stream());
+  }
   return launch_ntt_inv(log_len, a, ps, cx.stream());
 }
 
@@ -208,18 +291,28 @@ int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch, const uint
     set_last_error("p=%llu supports transforms up to length 2^%d", (unsigned long long)p, k);
     return kOutOfRange;
   }
-  if (log_len > 20) {
-    set_last_error("direct DFT limited to 2^20 points");
-    return kUnsupported;
+  if (batch <= 0) return kOk;
+  Context& cx = *ctx->cx;
+  const size_t n = (size_t)batch << log_len;
+  if (p < (1ull << 31) && log_len >= kMinLogN) {
+    // 31-bit primes: the fast u32 transforms on narrowed copies
+    Workspace ws(cx);
+    uint32_t *a, *b;
+    FPM_TRY(ws.get(n, &a));
+    FPM_TRY(ws.get(n, &b));
+    FPM_TRY(copy_narrow(in, a, n, cx.stream()));
+    FPM_TRY(fpm_ntt_u32(ctx, (uint32_t)p, log_len, batch, a, b, inverse));
+    return copy_widen(b, out, n, cx.stream());
   }
-  const uint64_t N = 1ull << log_len;
-  uint64_t omega = h_powmod(h_ntt_root(p), 1ull << (k - log_len), p);
-  uint64_t scale = 1;
-  if (inverse) {
-    omega = h_invmod(omega, p);
-    scale = h_invmod(N % p, p);
+  if (in == out) {
+    // the bit-reversal pass reads and writes different buffers
+    Workspace ws(cx);
+    uint64_t* tmp;
+    FPM_TRY(ws.get(n, &tmp));
+    FPM_CUDA_TRY(cudaMemcpyAsync(tmp, in, n * 8, cudaMemcpyDeviceToDevice, cx.stream()));
+    return ntt64(cx, p, log_len, batch, tmp, out, inverse);
   }
-  return launch_dft_direct(p, omega, (int)N, batch, in, out, scale, ctx->cx->stream());
+  return ntt64(cx, p, log_len, batch, in, out, inverse);
 }
 
 int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m, int k,

@@ -186,35 +186,55 @@ __global__ void rdeg_kernel(const T* M, int rows, int cols, int L, const int64_t
   if (lane == 0) out[row] = best == LLONG_MIN ? smin : best;
 }
 
-__global__ void dft_direct_kernel(uint64_t P, uint64_t Pni, uint64_t R2, uint64_t omega, int N,
-                                  int batch, const uint64_t* in, uint64_t* out, uint64_t scale) {
+// generic radix-2 NTT over any odd p < 2^62 (u64, Montgomery products):
+// bit-reversal copy, then log N global passes of DIT butterflies; twiddle
+// w^e = lo[e & mask] * hi[e >> h] (split table, normal form)
+__global__ void ntt64_bitrev_kernel(const uint64_t* in, uint64_t* out, int logn, long long batch) {
   pdl_wait();
-  const long long total = (long long)batch * N;
+  const long long N = 1LL << logn, total = batch * N;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const long long b = idx / N;
-    const int j = (int)(idx - b * N);
-    // w^j by square-and-multiply, then Horner-free accumulation sum in[t] (w^j)^t
-    uint64_t wj = 1, base = omega;
-    for (int e = j; e; e >>= 1) {
-      if (e & 1) wj = d_mulmod_any(wj, base, P, Pni, R2);
-      base = d_mulmod_any(base, base, P, Pni, R2);
+    const long long b = idx >> logn, j = idx & (N - 1);
+    const long long r = logn ? (long long)(__brevll((unsigned long long)j) >> (64 - logn)) : 0;
+    out[(b << logn) + r] = in[idx];
+  }
+}
+
+__global__ void ntt64_stage_kernel(uint64_t* x, int logn, int hb, long long batch, uint64_t P,
+                                   uint64_t Pni, uint64_t R2, const uint64_t* lo,
+                                   const uint64_t* hi, int h, uint64_t scale, int last) {
+  pdl_wait();
+  const long long N = 1LL << logn, half = N >> 1, total = batch * half;
+  const long long hh = 1LL << hb;
+  const long long mask = (1LL << h) - 1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long b = idx / half, q = idx - b * half;
+    const long long i = q & (hh - 1), g = q >> hb;
+    const long long u = (b << logn) + g * 2 * hh + i, v = u + hh;
+    const long long e = i << (logn - 1 - hb);  // w_{2hh}^i = w_N^(i N / 2hh)
+    uint64_t t = x[v];
+    if (e) {
+      const uint64_t w = d_mulmod_any(lo[e & mask], hi[e >> h], P, Pni, R2);
+      t = d_mulmod_any(t, w, P, Pni, R2);
     }
-    const uint64_t* v = in + b * N;
-    uint64_t acc = 0, pw = 1;
-    for (int t = 0; t < N; ++t) {
-      acc = d_addmod64(acc, d_mulmod_any(v[t], pw, P, Pni, R2), P);
-      pw = d_mulmod_any(pw, wj, P, Pni, R2);
+    const uint64_t s = x[u];
+    uint64_t a0 = d_addmod64(s, t, P), a1 = d_addmod64(s, P - t, P);
+    if (last && scale != 1) {
+      a0 = d_mulmod_any(a0, scale, P, Pni, R2);
+      a1 = d_mulmod_any(a1, scale, P, Pni, R2);
     }
-    out[idx] = d_mulmod_any(acc, scale, P, Pni, R2);
+    x[u] = a0;
+    x[v] = a1;
   }
 }
 
 }  // namespace
 
-int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64_t* in,
-                      uint64_t* out, uint64_t scale, cudaStream_t st) {
-  const long long total = (long long)batch * N;
+int launch_ntt64_generic(uint64_t p, uint64_t omega, int logn, int batch, const uint64_t* in,
+                         uint64_t* out, uint64_t scale, const uint64_t* lo, const uint64_t* hi,
+                         int h, cudaStream_t st) {
+  const long long N = 1LL << logn, total = (long long)batch * N;
   if (total <= 0) return kOk;
   CrtArgs tmp{};
   const uint32_t q1 = 2013265921u;
@@ -223,9 +243,20 @@ int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64
   const uint64_t R2 = (uint64_t)(R * R % p);
   long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  FPM_CUDA_TRY(launch_pdl(dft_direct_kernel, dim3((unsigned)blocks), dim3(256), 0, st, p, tmp.Pni, R2, omega, N, batch, in, out,
-                                                      scale));
+  FPM_CUDA_TRY(launch_pdl(ntt64_bitrev_kernel, dim3((unsigned)blocks), dim3(256), 0, st, in, out,
+                          logn, (long long)batch));
   FPM_LAUNCH_CHECK();
+  if (logn == 0 && scale != 1) {
+    set_last_error("internal: length-1 inverse");  // N^-1 = 1: never reached
+    return kInvalidArgument;
+  }
+  for (int hb = 0; hb < logn; ++hb) {
+    FPM_CUDA_TRY(launch_pdl(ntt64_stage_kernel, dim3((unsigned)blocks), dim3(256), 0, st, out,
+                            logn, hb, (long long)batch, p, tmp.Pni, R2, lo, hi, h, scale,
+                            hb == logn - 1 ? 1 : 0));
+    FPM_LAUNCH_CHECK();
+  }
+  (void)omega;
   return kOk;
 }
 

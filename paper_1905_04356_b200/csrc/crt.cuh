@@ -44,11 +44,14 @@ struct MiddleEntryArgs {
 };
 int launch_middle_entrywise(const MiddleEntryArgs& a, cudaStream_t st);
 
-// direct DFT over any odd p < 2^62 (u64 elements), natural order:
-// out[j] = sum_t in[t] w^(j t); inverse: w^-1 and scale by N^-1.  Used by the
-// public NTT entry point for lengths / moduli outside the fast 31-bit kernel.
-int launch_dft_direct(uint64_t p, uint64_t omega, int N, int batch, const uint64_t* in,
-                      uint64_t* out, uint64_t scale, cudaStream_t st);
+// radix-2 NTT over any odd p < 2^62 (u64 elements), natural order in and
+// out: out[j] = sum_t in[t] w^(j t); scale multiplies the last stage (N^-1
+// for the inverse).  lo / hi: split twiddle tables w^i (i < 2^h) and
+// w^(i 2^h) (i < N / 2^h), device, normal form.  The public NTT entry point
+// for moduli >= 2^31 (log N global passes; not a product-path kernel).
+int launch_ntt64_generic(uint64_t p, uint64_t omega, int logn, int batch, const uint64_t* in,
+                         uint64_t* out, uint64_t scale, const uint64_t* lo, const uint64_t* hi,
+                         int h, cudaStream_t st);
 
 // max trimmed entry length over a dense (rows*cols, L) matrix, written to
 // *out (device int); used for degree bookkeeping (polmat.py:95-104).

@@ -89,6 +89,16 @@ __host__ __device__ __forceinline__ long long eval_piece(int x0, long long e, lo
 }
 
 constexpr int kMinLogN = 5;
-constexpr int kMaxLogN = 15;
+constexpr int kMaxLogN = 15;  // single-CTA kernels; longer transforms: ntt_big.cu
+
+// transforms of 2^16 .. 2^30 points as passes over HBM (ntt_big.cu): blocked
+// eval layout (pblk_log 5) or natural order, any number of primes.  scratch:
+// n_entries * N * primes words (entry-major intermediate).
+class Context;
+bool ntt_big_ok(int logn);
+int launch_ntt_fwd_big(Context& cx, int logn, const NttFwdArgs& a, const PrimeSet& ps,
+                       uint32_t* scratch, cudaStream_t st);
+int launch_ntt_inv_big(Context& cx, int logn, const NttInvArgs& a, const PrimeSet& ps,
+                       uint32_t* scratch, cudaStream_t st);
 
 }  // namespace fpm

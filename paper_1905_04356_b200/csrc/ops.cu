@@ -136,9 +136,10 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   if (ec == 0 || C.len <= 0) return kOk;
   if (k == 0 || A.len <= 0 || B.len <= 0) return zero_out(C, ec, 0, C.len, st);
   if (logn < kMinLogN) logn = kMinLogN;  // a larger cyclic length is exact as well
-  if (logn > kMaxLogN) {
-    set_last_error("transform length 2^%d exceeds the single-CTA NTT limit 2^%d", logn,
-                   kMaxLogN);
+  // beyond one CTA (2^15): multi-pass transforms over HBM (ntt_big.cu)
+  const bool big = logn > kMaxLogN;
+  if (big && !ntt_big_ok(logn)) {
+    set_last_error("transform length 2^%d beyond the supported 2^30", logn);
     return kUnsupported;
   }
   const long long N = 1LL << logn;
@@ -186,6 +187,12 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   if (!cache) FPM_TRY(ws.get(r * N * ea, &EA));
   if (!cache_b || fold) FPM_TRY(ws.get(r * N * eb, &EB));
   FPM_TRY(ws.get(r * N * ec, &EC));
+  uint32_t* scratch = nullptr;  // long transforms: entry-major intermediate
+  if (big) {
+    long long most = ea > eb ? ea : eb;
+    if (ec > most) most = ec;
+    FPM_TRY(ws.get((size_t)r * N * most, &scratch));
+  }
 
   const int reduce_needed = direct ? 0 : (p > primes[r - 1] ? 1 : 0);
   // pointwise engine: int8 tensor cores where the contraction is a real dense
@@ -272,7 +279,16 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // both operands in one launch when their transforms are alike (persistent
   // grid: one tail wave instead of two)
   if (!a_cached) FPM_TRY(to_u32(fa, ea));
-  if (a_cached && b_cached) {
+  if (big) {
+    if (!a_cached) {
+      StageTimer t_(cx, "ntt_fwd_A");
+      FPM_TRY(launch_ntt_fwd_big(cx, logn, fa, ps, scratch, st));
+    }
+    if (!b_cached) {
+      StageTimer t_(cx, "ntt_fwd_B");
+      FPM_TRY(launch_ntt_fwd_big(cx, logn, fb, ps, scratch, st));
+    }
+  } else if (a_cached && b_cached) {
     // both evaluations reused
   } else if (a_cached) {
     StageTimer t_(cx, "ntt_fwd_B");
@@ -326,17 +342,21 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   ia.in = EC; ia.in_prime_stride = N * ec; ia.natural = 0; ia.pm = use_tc; ia.n_entries = (int)ec;
   ia.pblk_log = pq ? 2 : 5;
   ia.out_len = wlen; ia.off = (int)off; ia.scale = 1;
+  auto inverse = [&]() -> int {
+    return big ? launch_ntt_inv_big(cx, logn, ia, ps, scratch, st)
+               : launch_ntt_inv(logn, ia, ps, st);
+  };
   if (direct && !C.is64) {
     ia.out = (uint32_t*)C.ptr; ia.out_stride = C.stride; ia.out_prime_stride = 0;
     StageTimer t_(cx, "ntt_inv");
-    FPM_TRY(launch_ntt_inv(logn, ia, ps, st));
+    FPM_TRY(inverse());
   } else {
     uint32_t* R;
     FPM_TRY(ws.get((long long)r * ec * wlen, &R));
     ia.out = R; ia.out_stride = wlen; ia.out_prime_stride = ec * wlen;
     {
       StageTimer t_(cx, "ntt_inv");
-      FPM_TRY(launch_ntt_inv(logn, ia, ps, st));
+      FPM_TRY(inverse());
     }
     StageTimer t2_(cx, direct ? "widen" : "crt");
     if (direct) {

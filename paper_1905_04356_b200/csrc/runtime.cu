@@ -167,6 +167,11 @@ Context::~Context() {
     cudaFree(kv.second.itw);
     cudaFree(kv.second.itw_s);
   }
+  for (auto& kv : big_plans_) {
+    for (uint2* t : {kv.second.lo, kv.second.hi, kv.second.ilo, kv.second.ihi, kv.second.r1k,
+                     kv.second.ir1k})
+      cudaFree(t);
+  }
   if (pinned_) cudaFreeHost(pinned_);
   for (auto& a : aux_)
     if (a) cudaStreamDestroy(a);
@@ -420,6 +425,23 @@ bool pdl_enabled() { return option(kOptNoPdl) == 0; }
 
 int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   const Plan* pl = nullptr;
+  if (logn > 15) {
+    // long transforms keep their own split tables (big_plan, ntt_big.cu):
+    // no N-entry row table here, only the scalars
+    if (logn > h_two_adicity(p)) {
+      set_last_error("p=%u supports transforms up to length 2^%d, not 2^%d", p,
+                     h_two_adicity(p), logn);
+      return kOrderTooSmall;
+    }
+    *out = PrimeConst{};
+    out->p = p;
+    out->c32 = (uint32_t)(((uint64_t)1 << 32) % p);
+    out->mu = (uint64_t)((((u128)1) << 64) / p);
+    out->m58 = (uint32_t)((((u128)1) << 58) / p);
+    out->ninv = (uint32_t)h_invmod((1ull << logn) % p, p);
+    out->ninv_sh = h_shoup(out->ninv, p);
+    return kOk;
+  }
   FPM_TRY(plan(p, logn, &pl));
   out->p = p;
   out->c32 = (uint32_t)(((uint64_t)1 << 32) % p);

@@ -19,6 +19,16 @@ struct Plan {
   uint2 w32[16], iw32[16];
 };
 
+// long transforms (ntt_big.cu): split twiddle tables w_N^i (i < 2^h) and
+// w_N^(i 2^h), forward and inverse, plus the inner 1024-point DFT roots
+struct BigPlan {
+  uint32_t p = 0;
+  int h = 0;
+  uint2 *lo = nullptr, *hi = nullptr, *ilo = nullptr, *ihi = nullptr;
+  uint2 *r1k = nullptr, *ir1k = nullptr;
+  uint32_t ninv = 0, ninv_sh = 0;
+};
+
 class Context {
  public:
   explicit Context(int device);
@@ -35,6 +45,7 @@ class Context {
   int pinned(size_t bytes, void** out);
 
   int plan(uint32_t p, int logn, const Plan** out);
+  int big_plan(uint32_t p, int logn, const BigPlan** out);  // ntt_big.cu
 
   // copy streams of the pipelined host entry points (created on first use)
   int aux_stream(int i, cudaStream_t* out);
@@ -68,6 +79,7 @@ class Context {
   std::multimap<size_t, void*> free_;
   std::map<void*, size_t> used_;
   std::map<std::pair<uint32_t, int>, Plan> plans_;
+  std::map<std::pair<uint32_t, int>, BigPlan> big_plans_;
   void* pinned_ = nullptr;
   size_t pinned_bytes_ = 0;
 };

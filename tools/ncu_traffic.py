@@ -77,10 +77,12 @@ def parse(path, name):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             d["bytes"] = d.get("bytes", 0) + val * scale
         elif r["Metric Name"] == "gpu__time_duration.sum":
-            scale = {"nsecond": 1e-3, "usecond": 1, "msecond": 1e3}.get(unit, 1)
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3,
+                     "ms": 1e3}.get(unit, 1e-3)
             d["us"] = val * scale
-    ids = list(per)
-    # two identical products were captured: keep the second half of the launches
+    # own kernels only (input generation runs torch kernels); two identical
+    # products were captured: keep the second half of the launches
+    ids = [i for i in per if "fpm::" in per[i]["kernel"]]
     half = ids[len(ids) // 2:]
     launches = [per[i] for i in half]
     stages = collections.OrderedDict()
