@@ -205,7 +205,7 @@ def ntt_dense(x, p, log_len, inverse=False):
     h = _lib.context(x.device.index)
     L = _lib.lib()
     batch = x.shape[0]
-    if p < (1 << 31) and 5 <= log_len <= 15:
+    if p < (1 << 31):
         if x.dtype != torch.int32:
             raise ValueError("int32 storage expected for p < 2^31")
         out = torch.empty_like(x)
