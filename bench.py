@@ -356,17 +356,19 @@ def run_step(cfg, inputs, out=None):
     return dense.pmbasis_dense(inputs[0], cfg["sigma"], [0] * cfg["m"], cfg["p"])[0]
 
 
-def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
-    """Per-step CUDA-event time (ms list) with an L2 flush between steps."""
+def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None, step=None):
+    """Per-step CUDA-event time (ms list) with an L2 flush between steps.
+    step(cfg, inputs, out) defaults to one whole product / basis."""
     import torch
 
     from paper_1905_04356_b200 import _lib
 
+    run_step_ = step or run_step
     out = None
-    if cfg["kind"] == "mul":
+    if cfg["kind"] == "mul" and step is None:
         out = run_step(cfg, inputs)
     for _ in range(warmup):
-        run_step(cfg, inputs, out)
+        run_step_(cfg, inputs, out)
     torch.cuda.synchronize()
     times = []
     stages = {}
@@ -376,7 +378,7 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        run_step(cfg, inputs, out)
+        run_step_(cfg, inputs, out)
         e1.record()
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
@@ -387,7 +389,7 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
         for _ in range(min(steps, 3)):
             flush.zero_()
             _lib.profile(profile_h, True)
-            run_step(cfg, inputs, out)
+            run_step_(cfg, inputs, out)
             torch.cuda.synchronize()
             for name, ms in _lib.profile_records(profile_h):
                 stages.setdefault(name, []).append(ms)
@@ -395,17 +397,20 @@ def time_steps(cfg, inputs, steps, warmup, flush, profile_h=None):
     return times, stages, launches
 
 
-def e2e_mul(cfg, steps, warmup, seed):
+def e2e_mul(cfg, steps, warmup, seed, rank=0, world=1):
     """Same metric through the C ABI host entry (pinned host buffers): every
-    call uploads A and B and downloads C inside the timed region."""
+    call uploads A and B and downloads C inside the timed region.  On N > 1
+    ranks each rank runs its 2-D block (A row block x B column block)."""
     import torch
 
     from paper_1905_04356_b200 import _lib, dense
+    from paper_1905_04356_b200.parallel import block_of
 
     p = cfg["p"]
     A, B = make_inputs(cfg, "cuda", seed)
-    Ah = A.cpu().pin_memory()
-    Bh = B.cpu().pin_memory()
+    (r0, r1), (c0, c1) = block_of(rank, world, A.shape[0], B.shape[1])
+    Ah = A[r0:r1].contiguous().cpu().pin_memory()
+    Bh = B[:, c0:c1].contiguous().cpu().pin_memory()
     del A, B
     m, k, la = Ah.shape
     _, n, lb = Bh.shape
@@ -543,9 +548,36 @@ def bench_config(args, cfg, world):
         N, r = mul_plan(cfg)
         c.update({"N": N, "word_primes": r})
     c["l2"] = "flushed: 256 MiB write between timed steps (outside events); inputs > L2"
-    c["parallelism"] = (f"replicas x{world} (one independent product per rank)" if world > 1
-                        else "single GPU")
+    c["parallelism"] = parallelism(cfg, world)
     return c
+
+
+def split_mode(cfg, world):
+    """How a product shards over `world` GPUs: 'prime' for a
+    multi-prime product (one word prime per rank, residues gathered to rank
+    0 for the CRT), '2d' for a direct one (A-row x B-column blocks, C stays
+    sharded), None on one GPU or for PM-Basis (replicas only)."""
+    if world <= 1 or cfg["kind"] != "mul":
+        return None
+    return "prime" if mul_plan(cfg)[1] > 1 else "2d"
+
+
+def parallelism(cfg, world):
+    mode = split_mode(cfg, world)
+    if mode is None:
+        return "single GPU" if world <= 1 else f"replicas x{world} (one instance per rank)"
+    if mode == "prime":
+        return (f"prime split x{world}: word primes round-robin over ranks, residues gathered "
+                "(NCCL) to rank 0 for the CRT; one product per step (strong scaling)")
+    from paper_1905_04356_b200.parallel import grid_shape
+
+    gr, gc = grid_shape(world)
+    return (f"2-D blocks {gr}x{gc}: rank (i, j) multiplies A row block i by B column block j, "
+            "no collective, C stays sharded; one product per step (strong scaling)")
+
+
+def scaling_of(cfg, world):
+    return "strong" if split_mode(cfg, world) else "weak"
 
 
 def reference_arm(args, cfg, rank, world):
@@ -570,7 +602,7 @@ def reference_arm(args, cfg, rank, world):
         "metric": METRIC, "value": round(val, 4), "unit": "Gmodmul/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None,
+        "scaling": scaling_of(cfg, world), "vs_baseline": None,
         "dtype": "u32" if cfg["p"] < (1 << 31) else "u64",
         "data": "synthetic (seeded uniform coefficients in [0,p), numpy PCG64)",
         "config": bench_config(args, cfg, world),
@@ -681,7 +713,20 @@ def main():
     from paper_1905_04356_b200 import _lib
 
     h = _lib.context(local)
-    inputs = make_inputs(cfg, device, 1000 + rank)
+    mode = split_mode(cfg, world)
+    # replicas: every rank its own inputs; a split product: the same inputs
+    inputs = make_inputs(cfg, device, 1000 + (0 if mode else rank))
+    step = None
+    if mode == "2d":
+        from paper_1905_04356_b200.parallel import pm_mul_2d
+
+        def step(cfg_, inp, out):
+            return pm_mul_2d(inp[0], inp[1], cfg_["p"], rank, world)
+    elif mode == "prime":
+        from paper_1905_04356_b200.parallel import pm_mul_prime_split
+
+        def step(cfg_, inp, out):
+            return pm_mul_prime_split(inp[0], inp[1], cfg_["p"], dst=0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
     clocks = Clocks(local)
     if dist is not None:
@@ -689,7 +734,7 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     times, stages, launches = time_steps(cfg, inputs, args.steps, args.warmup, flush,
-                                         profile_h=h)
+                                         profile_h=h, step=step)
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = sum(times)
@@ -703,18 +748,41 @@ def main():
         work, sbytes, N, r = mul_work(cfg)
     else:
         work, sbytes, N, r = pmbasis_work(cfg), {}, None, None
-    value = world * work * args.steps / (total_ms * 1e-3) / 1e9
+    # replicas: every rank did a whole unit; a split product: one unit per step
+    units = 1 if mode else world
+    value = units * work * args.steps / (total_ms * 1e-3) / 1e9
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Gmodmul/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": scaling_of(cfg, world), "vs_baseline": None,
         "dtype": "u32" if cfg["p"] < (1 << 31) else "u64",
         "data": "synthetic (seeded uniform coefficients in [0,p), torch.Generator)",
         "config": bench_config(args, cfg, world),
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if mode == "2d" and not args.no_extras:
+        # the optional exchange: one all_gather of the C blocks (NCCL) for a
+        # consumer that needs all of C on every rank (not in the timed steps)
+        from paper_1905_04356_b200.parallel import gather_blocks
+
+        Cb = step(cfg, inputs, None)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record()
+        C = gather_blocks(Cb, cfg["m"], cfg["n"])
+        g1.record()
+        g1.synchronize()
+        gms = torch.tensor([g0.elapsed_time(g1)], device=device)
+        dist.all_reduce(gms, op=dist.ReduceOp.MAX)
+        line["exchange"] = {"kind": "all_gather of the C blocks (NCCL), once after the timed "
+                                    "steps", "ms": round(float(gms.item()), 4),
+                            "bytes_per_rank_sent": Cb.numel() * Cb.element_size(),
+                            "bytes_per_rank_received": C.numel() * C.element_size()}
+        del C, Cb
     del inputs
     # roofline of the dominant kernel class, CUDA events inside the timed region
     if stages:
@@ -729,19 +797,26 @@ def main():
         # device-timed value); the slowest rank's median sets the job time
         err = None
         try:
-            med, bi, bo = e2e_mul(cfg, max(3, min(args.steps, 10)), 2, 7 + rank)
+            med, bi, bo = e2e_mul(cfg, max(3, min(args.steps, 10)), 2, 7 + (0 if mode else rank),
+                                  rank if mode else 0, world if mode else 1)
         except Exception as exc:
             med, bi, bo, err = float("inf"), 0, 0, f"{type(exc).__name__}: {exc}"
         if dist is not None:
             t = torch.tensor([med], device=device, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             med = float(t.item())
+        if dist is not None:
+            tb = torch.tensor([bi, bo], device=device, dtype=torch.float64)
+            dist.all_reduce(tb)
+            bi, bo = int(tb[0].item()), int(tb[1].item())
         if err is None and math.isfinite(med):
-            line["e2e"] = {"value": round(world * work / med / 1e9, 3), "unit": "Gmodmul/s",
-                           "h2d_bytes_per_step": world * bi, "d2h_bytes_per_step": world * bo,
+            line["e2e"] = {"value": round(units * work / med / 1e9, 3), "unit": "Gmodmul/s",
+                           "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                            "ms_per_step": round(med * 1e3, 4), "n_gpus": world,
-                           "path": "fpm_polmat_mul_host (C ABI, pinned host buffers), "
-                                   "one product per rank, max over ranks"}
+                           "path": "fpm_polmat_mul_host (C ABI, pinned host buffers); "
+                                   + ("each rank its 2-D block of one product"
+                                      if mode else "one product per rank")
+                                   + ", max over ranks"}
         else:
             line["e2e"] = {"error": err or "a rank failed its host-buffer product"}
     if rank == 0 and not args.no_extras and cfg["kind"] == "mul" and world == 1:

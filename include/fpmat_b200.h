@@ -114,6 +114,22 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes,
                         const void* A_host, int m, int k, int la,
                         const void* B_host, int n, int lb, void* C_host);
 
+/* ---- multi-prime pieces (for splitting a product over GPUs by prime,
+ *      SURVEY.md 8e) -------------------------------------------------------
+ * fpm_product_primes: the word primes fpm_polmat_mul runs a product of
+ * A (m x k, length la) by B (k x n, length lb) over -- {p} for a 31-bit NTT
+ * prime of enough two-adicity, else the CRT set (the reference computes the
+ * same unique product geometrically, polmat.py:311-346).
+ * fpm_split_residues: out[z][i] = in[i] mod primes[z] (device, n elements).
+ * fpm_crt_combine: residues [r][entries][len] (device) -> out mod p, the
+ * Garner recombination fpm_polmat_mul applies (elem_bytes 4 or 8). */
+int fpm_product_primes(uint64_t p, int k, int la, int lb, uint32_t* primes, int cap,
+                       int* count);
+int fpm_split_residues(fpm_context* ctx, int elem_bytes, const void* in_dev, long long n,
+                       const uint32_t* primes, int r, uint32_t* out_dev);
+int fpm_crt_combine(fpm_context* ctx, uint64_t p, int elem_bytes, const uint32_t* primes, int r,
+                    const uint32_t* res_dev, long long entries, int len, void* out_dev);
+
 /* ---- Multiplier (polmat.Multiplier / multiplier_precompute /
  *      multiplier_apply, polmat.py:550-610) ------------------------------------
  * A fixed left factor A (m x k, length la; copied on create) whose forward

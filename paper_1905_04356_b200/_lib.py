@@ -88,6 +88,12 @@ def lib():
             "fpm_ntt_u32": (i32, [vp, u32, i32, i32, vp, vp, i32]),
             "fpm_ntt_u64": (i32, [vp, u64, i32, i32, vp, vp, i32]),
             "fpm_polmat_mul": (i32, [vp, u64, i32, vp, i32, i32, i32, vp, i32, i32, vp]),
+            "fpm_product_primes": (i32, [u64, i32, i32, i32, ctypes.POINTER(ctypes.c_uint32),
+                                         i32, pint]),
+            "fpm_split_residues": (i32, [vp, i32, vp, i64, ctypes.POINTER(ctypes.c_uint32), i32,
+                                         vp]),
+            "fpm_crt_combine": (i32, [vp, u64, i32, ctypes.POINTER(ctypes.c_uint32), i32, vp,
+                                      i64, i32, vp]),
             "fpm_polmat_mul_host": (i32, [vp, u64, i32, vp, i32, i32, i32, vp, i32, i32, vp]),
             "fpm_polmat_middle": (i32, [vp, u64, i32, vp, i32, i32, i32, vp, i32, i32, i64,
                                         i32, i32, vp]),

@@ -81,6 +81,16 @@ int copy_narrow(const uint64_t* in, uint32_t* out, long long n, cudaStream_t st)
   return kOk;
 }
 
+__global__ void residues_kernel(const void* in, int in64, long long n, PrimeSet ps,
+                                uint32_t* out) {
+  pdl_wait();
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const uint64_t v = in64 ? ((const unsigned long long*)in)[i] : ((const uint32_t*)in)[i];
+    for (int z = 0; z < ps.count; ++z) out[(long long)z * n + i] = d_red64(v, ps.pr[z].p, ps.pr[z].mu);
+  }
+}
+
 // modring.ntt_forward / ntt_inverse for any prime (u64 generic transform):
 // split twiddle tables built on the host per call (API path, not hot)
 int ntt64(Context& cx, uint64_t p, int log_len, int batch, const uint64_t* in, uint64_t* out,
@@ -313,6 +323,61 @@ int fpm_ntt_u64(fpm_context* ctx, uint64_t p, int log_len, int batch, const uint
     return ntt64(cx, p, log_len, batch, tmp, out, inverse);
   }
   return ntt64(cx, p, log_len, batch, in, out, inverse);
+}
+
+int fpm_product_primes(uint64_t p, int k, int la, int lb, uint32_t* primes, int cap,
+                       int* count) {
+  if (!primes || !count || k < 0 || la <= 0 || lb <= 0) return kInvalidArgument;
+  FPM_TRY(check_elem(p, 8));
+  int logn = ceil_log2_min1((long long)la + lb - 1);
+  if (logn < kMinLogN) logn = kMinLogN;
+  uint32_t q[kMaxPrimes];
+  int r = 0;
+  FPM_TRY(select_primes(p, k, la, lb, logn, q, &r));
+  *count = r;
+  if (r > cap) {
+    set_last_error("%d primes, room for %d", r, cap);
+    return kInvalidArgument;
+  }
+  for (int i = 0; i < r; ++i) primes[i] = q[i];
+  return kOk;
+}
+
+int fpm_split_residues(fpm_context* ctx, int elem_bytes, const void* in_dev, long long n,
+                       const uint32_t* primes, int r, uint32_t* out_dev) {
+  FPM_TRY(bind_device(ctx));
+  if ((elem_bytes != 4 && elem_bytes != 8) || n < 0 || r < 1 || r > kMaxPrimes || !primes)
+    return kInvalidArgument;
+  if (n == 0) return kOk;
+  PrimeSet ps{};
+  ps.count = r;
+  for (int z = 0; z < r; ++z) {
+    if (primes[z] <= 2 || primes[z] >= (1u << 31)) {
+      set_last_error("residue primes must satisfy 2 < q < 2^31");
+      return kOutOfRange;
+    }
+    ps.pr[z].p = primes[z];
+    ps.pr[z].mu = (uint64_t)((((u128)1) << 64) / primes[z]);
+  }
+  FPM_CUDA_TRY(launch_pdl(residues_kernel, dim3(copy_grid(n)), dim3(256), 0, ctx->cx->stream(),
+                          in_dev, elem_bytes == 8 ? 1 : 0, n, ps, out_dev));
+  FPM_LAUNCH_CHECK();
+  return kOk;
+}
+
+int fpm_crt_combine(fpm_context* ctx, uint64_t p, int elem_bytes, const uint32_t* primes, int r,
+                    const uint32_t* res_dev, long long entries, int len, void* out_dev) {
+  FPM_TRY(bind_device(ctx));
+  FPM_TRY(check_elem(p, elem_bytes));
+  if (!primes || r < 1 || r > kMaxPrimes || entries < 0 || len < 0 || entries > (1LL << 31))
+    return kInvalidArgument;
+  if (entries == 0 || len == 0) return kOk;
+  CrtArgs ca{};
+  crt_prepare(ca, primes, r, p);
+  ca.res = res_dev; ca.res_prime_stride = entries * len; ca.res_stride = len;
+  ca.n_entries = (int)entries; ca.len = len;
+  ca.out = out_dev; ca.out64 = elem_bytes == 8 ? 1 : 0; ca.out_stride = len;
+  return launch_crt(ca, ctx->cx->stream());
 }
 
 int fpm_polmat_mul(fpm_context* ctx, uint64_t p, int elem_bytes, const void* A, int m, int k,

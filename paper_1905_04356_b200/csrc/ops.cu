@@ -129,6 +129,37 @@ int matrix_degrees(Context& cx, const void* M1, int is64, long long e1, int L1, 
   return kOk;
 }
 
+int select_primes(uint64_t p, int k, long long la, long long lb, int logn, uint32_t* primes,
+                  int* count) {
+  int r = 0;
+  if (direct_ok(p, logn)) {
+    primes[r++] = (uint32_t)p;
+    *count = r;
+    return kOk;
+  }
+  // exact integer cyclic convolution needs prod(q) > bound
+  const long long N = 1LL << logn;
+  const bool fold = lb > N;
+  const double nfold = fold ? std::ceil((double)lb / (double)N) : 1.0;
+  double terms = (double)la;
+  if (!fold && lb < terms) terms = (double)lb;
+  if (terms > (double)N) terms = (double)N;
+  const double lg = std::log2((double)(k > 0 ? k : 1)) + std::log2(terms) + std::log2(nfold) +
+                    2.0 * std::log2((double)(p - 1)) + 2.0;
+  double have = 0.0;
+  for (int i = 0; i < kNumCrtPrimes && have <= lg; ++i) {
+    if (h_two_adicity(kCrtPrimes[i]) < logn) continue;
+    primes[r++] = kCrtPrimes[i];
+    have += std::log2((double)kCrtPrimes[i]);
+  }
+  if (have <= lg) {
+    set_last_error("coefficient bound 2^%.1f exceeds the multi-prime capacity", lg);
+    return kUnsupported;
+  }
+  *count = r;
+  return kOk;
+}
+
 int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef B,
                    int logn, long long off, OutRef C, EvalCache* cache, EvalCache* cache_b) {
   cudaStream_t st = cx.stream();
@@ -154,28 +185,8 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   // ---- prime selection -----------------------------------------------------
   uint32_t primes[kMaxPrimes];
   int r = 0;
-  bool direct = direct_ok(p, logn);
-  if (direct) {
-    primes[r++] = (uint32_t)p;
-  } else {
-    // exact integer cyclic convolution needs prod(q) > bound
-    const double nfold = fold ? std::ceil((double)B.len / (double)N) : 1.0;
-    double terms = (double)A.len;
-    if (!fold && B.len < terms) terms = (double)B.len;
-    if (terms > (double)N) terms = (double)N;
-    const double lg = std::log2((double)k) + std::log2(terms) + std::log2(nfold) +
-                      2.0 * std::log2((double)(p - 1)) + 2.0;
-    double have = 0.0;
-    for (int i = 0; i < kNumCrtPrimes && have <= lg; ++i) {
-      if (h_two_adicity(kCrtPrimes[i]) < logn) continue;
-      primes[r++] = kCrtPrimes[i];
-      have += std::log2((double)kCrtPrimes[i]);
-    }
-    if (have <= lg) {
-      set_last_error("coefficient bound 2^%.1f exceeds the multi-prime capacity", lg);
-      return kUnsupported;
-    }
-  }
+  const bool direct = direct_ok(p, logn);
+  FPM_TRY(select_primes(p, k, A.len, B.len, logn, primes, &r));
   PrimeSet ps;
   ps.count = r;
   for (int i = 0; i < r; ++i) FPM_TRY(cx.prime_const(primes[i], logn, &ps.pr[i]));

@@ -66,6 +66,12 @@ int ceil_log2_min1(long long need);
 // device-side degree of a dense matrix (max trimmed length - 1), synchronous
 // deg = max entry degree (-1 for zero); synchronizes the context stream once
 // (the reference's dispatch depends on the degrees, polmat.py:477-497)
+// the word primes a product A (m x k, length la) * B (k x n, length lb) at
+// cyclic length 2^logn runs over: {p} when p is a 31-bit NTT prime of
+// two-adicity >= logn, else the CRT set whose product bounds the integer
+// convolution (kCrtPrimes order)
+int select_primes(uint64_t p, int k, long long la, long long lb, int logn, uint32_t* primes,
+                  int* count);
 int matrix_degree(Context& cx, const void* M, int is64, long long entries, int L, int* deg);
 int matrix_degrees(Context& cx, const void* M1, int is64, long long e1, int L1, const void* M2,
                    long long e2, int L2, int* deg1, int* deg2);

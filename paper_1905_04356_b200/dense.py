@@ -266,3 +266,45 @@ class DenseMultiplier:
             self.close()
         except Exception:
             pass
+
+
+# ---- multi-prime pieces (parallel.pm_mul_prime_split) -------------
+
+def product_primes(p, k, la, lb):
+    """Word primes fpm_polmat_mul uses for A (.., k, la) * B (k, .., lb) mod p
+    ([p] for a direct 31-bit NTT prime)."""
+    buf = (ctypes.c_uint32 * 8)()
+    cnt = ctypes.c_int(0)
+    _lib.check(_lib.lib().fpm_product_primes(p, k, la, lb, buf, 8, ctypes.byref(cnt)),
+               "fpm_product_primes")
+    return [int(buf[i]) for i in range(cnt.value)]
+
+
+def split_residues(X, p, primes):
+    """X (device tensor of values mod p) -> (len(primes), *X.shape) int32
+    residues X mod q (fpm_split_residues)."""
+    import torch
+
+    _check_tensor(X, p, "X")
+    X = X.contiguous()
+    out = torch.empty((len(primes),) + tuple(X.shape), dtype=torch.int32, device=X.device)
+    qs = (ctypes.c_uint32 * len(primes))(*primes)
+    h = _lib.context(X.device.index)
+    _lib.check(_lib.lib().fpm_split_residues(h, elem_bytes_for(p), X.data_ptr(), X.numel(), qs,
+                                             len(primes), out.data_ptr()), "fpm_split_residues")
+    return out
+
+
+def crt_combine(R, p, primes):
+    """Residues R (len(primes), m, n, L) int32 on the device -> (m, n, L) mod p
+    (fpm_crt_combine, the Garner step of the multi-prime product)."""
+    import torch
+
+    r, m, n, L = R.shape
+    R = R.contiguous()
+    out = torch.empty((m, n, L), dtype=torch_dtype(p), device=R.device)
+    qs = (ctypes.c_uint32 * r)(*primes)
+    h = _lib.context(R.device.index)
+    _lib.check(_lib.lib().fpm_crt_combine(h, p, elem_bytes_for(p), qs, r, R.data_ptr(), m * n, L,
+                                          out.data_ptr()), "fpm_crt_combine")
+    return out

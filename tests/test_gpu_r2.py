@@ -1,0 +1,116 @@
+"""Round-2 goldens from the unmodified reference (tests/golden/make_golden_r2.py):
+PM-Basis over a 60-bit prime of two-adicity 1 (entrywise middle products
+on strided bases) and interpolant bases whose points repeat a residue."""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_1905_04356_b200 as F
+from paper_1905_04356_b200 import dense
+
+pytestmark = pytest.mark.gpu
+
+with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "r2.json")) as f:
+    R2 = json.load(f)
+
+
+def _draw_pmb(rec):
+    rng = random.Random(rec["seed"])
+    p, m, n, order = rec["p"], rec["m"], rec["n"], rec["order"]
+    return np.array([[[rng.randrange(p) for _ in range(order)] for _ in range(n)]
+                     for _ in range(m)], dtype=np.uint64)
+
+
+def _draw_ib(rec):
+    rng = random.Random(rec["seed"])
+    p, m, n, order = rec["p"], rec["m"], rec["n"], rec["order"]
+    E = [[[rng.randrange(p) for _ in range(n)] for _ in range(m)] for _ in range(order)]
+    alpha = [1, 1 + p] + rng.sample(range(1, p), order - 2)
+    return E, alpha
+
+
+@pytest.mark.parametrize("idx", range(len(R2["pmbasis"])))
+def test_pmbasis_p60_two_adicity_1(idx):
+    rec = R2["pmbasis"][idx]
+    p = rec["p"]
+    Fm = _draw_pmb(rec)
+    P, _ = dense.pmbasis_dense(dense.to_device(Fm, p), rec["order"], rec["s"], p, T=rec["T"])
+    got = F.polmat.from_dense(F.field_new(p), dense.to_numpy(P, p).astype(object),
+                              ncols=rec["m"])
+    assert got.rows == rec["P"]
+
+
+@pytest.mark.parametrize("idx", range(len(R2["intbasis"])))
+def test_intbasis_repeated_residue(idx):
+    rec = R2["intbasis"][idx]
+    E, alpha = _draw_ib(rec)
+    assert alpha[0] % rec["p"] == alpha[1] % rec["p"]
+    ctx = F.field_new(rec["p"])
+    fn = getattr(F, rec["fn"])
+    P = fn(E, alpha, [0] * rec["m"], ctx)
+    assert P.rows == rec["P"]
+
+
+def _one_rank_nccl():
+    import socket
+
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1)
+
+
+def test_prime_split_pieces_match_the_product():
+    """cfg3's shape through the split pieces on one GPU: residues per word
+    prime, one direct product per prime, Garner -- equal to pm_mul_dense
+    (which fuses the same steps), and through pm_mul_prime_split on a
+    one-rank NCCL group."""
+    from paper_1905_04356_b200 import parallel
+
+    p = (1 << 60) - 93
+    rng = np.random.default_rng(3)
+    A = rng.integers(0, p, size=(16, 16, 2048), dtype=np.uint64)
+    B = rng.integers(0, p, size=(16, 16, 2048), dtype=np.uint64)
+    A[0, 0] = p - 1
+    Ad, Bd = dense.to_device(A, p), dense.to_device(B, p)
+    want = dense.to_numpy(dense.pm_mul_dense(Ad, Bd, p), p)
+    primes = dense.product_primes(p, 16, 2048, 2048)
+    assert len(primes) == 5
+    Ar, Br = dense.split_residues(Ad, p, primes), dense.split_residues(Bd, p, primes)
+    import torch
+
+    R = torch.stack([dense.pm_mul_dense(Ar[z].contiguous(), Br[z].contiguous(), q)
+                     for z, q in enumerate(primes)])
+    got = dense.to_numpy(dense.crt_combine(R, p, primes), p)
+    assert np.array_equal(got, want)
+    _one_rank_nccl()
+    C = parallel.pm_mul_prime_split(Ad, Bd, p, dst=0)
+    assert np.array_equal(dense.to_numpy(C, p), want)
+
+
+def test_2d_blocks_on_nccl():
+    from paper_1905_04356_b200 import parallel
+
+    p = 2013265921
+    rng = np.random.default_rng(4)
+    A = rng.integers(0, p, size=(40, 8, 300), dtype=np.uint64)
+    B = rng.integers(0, p, size=(8, 24, 200), dtype=np.uint64)
+    Ad, Bd = dense.to_device(A, p), dense.to_device(B, p)
+    want = dense.to_numpy(dense.pm_mul_dense(Ad, Bd, p), p)
+    _one_rank_nccl()
+    C = parallel.pm_mul_sharded(Ad, Bd, p)
+    assert np.array_equal(dense.to_numpy(C, p), want)
+    # every block of a 2 x 4 grid, computed here one after another
+    for r in range(8):
+        Cb = parallel.pm_mul_2d(Ad, Bd, p, r, 8)
+        (a, b), (c, d) = parallel.block_of(r, 8, 40, 24)
+        assert np.array_equal(dense.to_numpy(Cb, p), want[a:b, c:d])
