@@ -152,6 +152,7 @@ enum Option : int {
   kOptNttPmScatter,       // "ntt_pm_scatter": one transform per CTA in PM layout
   kOptPmbasisLeaf,        // "pmbasis_leaf": cap of the device leaf order (default 8)
   kOptPmbasisHostSync,    // "pmbasis_host_sync": host-synchronised recursion
+  kOptNttNoMma,           // "ntt_no_mma": no tensor-core NTT (ntt_mma.cu)
   kOptCount
 };
 long long option(Option o);
@@ -189,6 +190,7 @@ struct PrimeConst {
   uint2 iw32[16];    // inverse roots
   uint2 sc[4];       // (2^(8q) mod p, Shoup), q = 0..3: limb scaling (tc_pointwise.cu)
   uint32_t m58;      // floor(2^58 / p): reduction of < 2^56 limb sums (d_red56)
+  const uint8_t* mma;  // tensor-core NTT tables (N = 4096, 2^30 < p < 2^31; ntt_mma.cu)
 };
 
 constexpr int kMaxPrimes = 8;

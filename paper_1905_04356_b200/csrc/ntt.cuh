@@ -81,6 +81,12 @@ bool ntt_tma_inv_ok(int logn, const NttInvArgs& a);
 int launch_ntt_fwd_tma(int logn, const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
 int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// forward transforms on the int8 tensor cores (ntt_mma.cu): N = 4096, one
+// prime 2^30 < p < 2^31, point-major output in the same DIF point order as
+// the kernels above (launch_ntt_fwd picks it when it applies)
+bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps);
+int launch_ntt_fwd_mma(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 // word offset of the 16-byte piece holding points x0 .. x0+3 (x0 % 4 == 0)
 // of entry e in the blocked eval layout E[N / 2^pl][n_entries][2^pl]
 __host__ __device__ __forceinline__ long long eval_piece(int x0, long long e, long long n_entries,

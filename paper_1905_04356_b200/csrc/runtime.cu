@@ -304,6 +304,12 @@ int Context::plan(uint32_t p, int logn, const Plan** out) {
   }
   pl.ninv = (uint32_t)h_invmod(N % p, p);
   pl.ninv_sh = h_shoup(pl.ninv, p);
+  if (logn == 12 && p > (1u << 30) && p < (1u << 31)) {
+    std::vector<uint8_t> tab;
+    mma_ntt_tables(p, (uint32_t)omega, &tab);
+    FPM_CUDA_TRY(cudaMalloc(&pl.mma, tab.size()));
+    FPM_CUDA_TRY(cudaMemcpy(pl.mma, tab.data(), tab.size(), cudaMemcpyHostToDevice));
+  }
   auto res = plans_.emplace(key, pl);
   *out = &res.first->second;
   return kOk;
@@ -386,7 +392,7 @@ struct OptDef {
 const OptDef kOptDefs[kOptCount] = {
     {"no_pdl", 0},      {"host_blocks", 0},   {"no_chirp", 0},     {"ntt_generic", 0},
     {"ntt_no_tma", 0},  {"ntt_no_small", 0},  {"ntt_pm_lsu", 0},   {"ntt_pm_scatter", 0},
-    {"pmbasis_leaf", 8}, {"pmbasis_host_sync", 0},
+    {"pmbasis_leaf", 8}, {"pmbasis_host_sync", 0}, {"ntt_no_mma", 0},
 };
 std::atomic<long long> g_opt[kOptCount] = {};
 std::atomic<bool> g_opt_init{false};
@@ -456,6 +462,7 @@ int Context::prime_const(uint32_t p, int logn, PrimeConst* out) {
   out->tw = pl->tw;
   out->itw = pl->itw;
   out->itw_s = pl->itw_s;
+  out->mma = pl->mma;
   for (int e = 0; e < 16; ++e) {
     out->w32[e] = pl->w32[e];
     out->iw32[e] = pl->iw32[e];

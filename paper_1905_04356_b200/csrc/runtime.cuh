@@ -17,6 +17,7 @@ struct Plan {
   uint2* itw_s = nullptr;  // device, N entries: itw * N^-1 (last inverse pass, ntt_tma.cu)
   uint32_t ninv = 0, ninv_sh = 0;
   uint2 w32[16], iw32[16];
+  uint8_t* mma = nullptr;  // device tables of the tensor-core NTT (ntt_mma.cu), N = 4096
 };
 
 // long transforms (ntt_big.cu): split twiddle tables w_N^i (i < 2^h) and
@@ -28,6 +29,9 @@ struct BigPlan {
   uint2 *r1k = nullptr, *ir1k = nullptr;
   uint32_t ninv = 0, ninv_sh = 0;
 };
+
+// host tables of the tensor-core NTT for (p, N = 4096) (ntt_mma.cu)
+void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out);
 
 class Context {
  public:
