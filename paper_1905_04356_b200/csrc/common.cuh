@@ -153,6 +153,7 @@ enum Option : int {
   kOptPmbasisLeaf,        // "pmbasis_leaf": cap of the device leaf order (default 8)
   kOptPmbasisHostSync,    // "pmbasis_host_sync": host-synchronised recursion
   kOptNttNoMma,           // "ntt_no_mma": no tensor-core NTT (ntt_mma.cu)
+  kOptTcNoPair,           // "tc_no_pair": tc_grouped instead of tc_pair for 128 < m <= 256
   kOptCount
 };
 long long option(Option o);

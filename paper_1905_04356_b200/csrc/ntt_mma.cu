@@ -159,18 +159,6 @@ __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int
       "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-// mbarrier wait that suspends the warp until the phase completes (time hint
-// 1 ms) instead of re-issuing try_wait: waiting workers leave issue slots to
-// the warps that have work
-__device__ __forceinline__ void wait_sleep(uint64_t* mbar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred done;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, 1000000;\n\t"
-      "@!done bra WAIT_%=;\n\t}\n" ::"r"(tc::smem_u32(mbar)),
-      "r"(parity)
-      : "memory");
-}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"

@@ -337,7 +337,11 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
     ta.A = EA; ta.B = EB; ta.C = EC; ta.m = m; ta.k = k; ta.n = n; ta.npts = (int)N;
     ta.a_ps = N * ea; ta.b_ps = N * eb; ta.c_ps = N * ec;
     StageTimer t_(cx, "pointwise_tc");
-    if (grouped)
+    bool pair = grouped && option(kOptTcNoPair) == 0;
+    for (int i = 0; i < r && pair; ++i) pair = tc_pair_applicable(m, k, n, primes[i]);
+    if (pair)
+      FPM_TRY(launch_tc_pair(ta, ps, st));
+    else if (grouped)
       FPM_TRY(launch_tc_grouped(ta, ps, st));
     else
       FPM_TRY(launch_tc_pointwise(ta, ps, st));

@@ -112,6 +112,18 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t addr, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// wait that suspends the warp until the phase completes (time hint 1 ms)
+// instead of re-issuing try_wait: many-warp roles waiting on the MMA or TMA
+// leave their issue slots to the warps with work
+__device__ __forceinline__ void mbar_wait_sleep_a(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1, 1000000;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
 // polling wait (test_wait, never suspends): for the single-thread TMA / MMA
 // roles on the latency-critical path
 __device__ __forceinline__ void mbar_wait_spin(uint32_t addr, uint32_t parity) {

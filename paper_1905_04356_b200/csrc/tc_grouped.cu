@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g > g_hi) break;
           RingPos& r = u ? sp1 : sp0;
           const int slot = r.idx * G + g;
-          tc::mbar_wait_a(a_afull + 8 * slot, r.ph);
+          tc::mbar_wait_sleep_a(a_afull + 8 * slot, r.ph);
           tc::fence_after_sync();
           const int il = 32 * q + lane - g * a.mp;  // row within the point's tile
           const int i = mt * 128 + il;
@@ -263,11 +263,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t w1 = pc.sc[1].x, w1p = pc.sc[1].y, w2 = pc.sc[2].x, w2p = pc.sc[2].y;
       const uint32_t w3 = pc.sc[3].x, w3p = pc.sc[3].y;
       for (int ch = 0; ch < nch; ++ch, st.next(NS)) {
-        tc::mbar_wait_a(a_full + 8 * st.idx, st.ph);
+        tc::mbar_wait_sleep_a(a_full + 8 * st.idx, st.ph);
         const uint32_t* raw = reinterpret_cast<const uint32_t*>(smem + kOffRaw + st.idx * kRawB);
         {
           RingPos r = br;
-          for (int u = 0; u < G; ++u, r.next(nring)) tc::mbar_wait_a(a_bempty + 8 * r.idx, r.ph ^ 1u);
+          for (int u = 0; u < G; ++u, r.next(nring)) tc::mbar_wait_sleep_a(a_bempty + 8 * r.idx, r.ph ^ 1u);
         }
         for (int task = ct; task < G * kTasks; task += kConvThreads) {
           const int gg = task / kTasks, tt = task - gg * kTasks;

@@ -26,6 +26,10 @@ int launch_tc_pointwise(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 bool tc_grouped_applicable(int m, int k, int n, uint32_t p);
 int launch_tc_grouped(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
 
+// 128 < m <= 256: both M tiles of a point share one built B tile (tc_pair.cu)
+bool tc_pair_applicable(int m, int k, int n, uint32_t p);
+int launch_tc_pair(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
+
 // m <= 32 on the point-quad eval layout X[t/4][entry][t%4] (tc_pq.cu)
 bool tc_pq_applicable(int m, int k, int n, int npts, uint32_t p);
 int launch_tc_pq(const TcArgs& a, const PrimeSet& ps, cudaStream_t st);
