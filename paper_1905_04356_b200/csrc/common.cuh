@@ -154,6 +154,7 @@ enum Option : int {
   kOptPmbasisHostSync,    // "pmbasis_host_sync": host-synchronised recursion
   kOptNttNoMma,           // "ntt_no_mma": no tensor-core NTT (ntt_mma.cu)
   kOptTcNoPair,           // "tc_no_pair": tc_grouped instead of tc_pair for 128 < m <= 256
+  kOptTcPair1,            // "tc_pair1": one-SM tc_pair instead of the CTA-pair kernel
   kOptCount
 };
 long long option(Option o);
