@@ -65,10 +65,15 @@ namespace fpm {
 //   [0, 4K)      DFT16 B operand (K-major SWIZZLE_NONE, LBO 128, SBO 512)
 //   [4K, 8K)     the same with bit-reversed output columns (pass 3)
 //   [8K, 40K)    twiddles: row m < 256, column j < 16: w^(m j)
+//   [40K, 44K)   inverse DFT16 B operand, K rows in bit-reversed input order
+//   [44K, 48K)   the same times N^-1 (inverse pass 3)
+//   [48K, 80K)   inverse twiddles: row 16 k0 + a, column b: w^-(k0 (a + 16 b))
 // twiddle rows hold 16 (w, floor(w 2^32 / p)) pairs = 128 bytes; the 16-byte
 // chunk c of row m is stored at chunk c ^ (m & 7) (conflict-free row reads).
 constexpr uint32_t kMmaTabB = 0, kMmaTabBr = 4096, kMmaTabTw = 8192;
-constexpr uint32_t kMmaTabBytes = 8192 + 32768;
+constexpr uint32_t kMmaTabInv = 40960;  // inverse tables: B, B N^-1, twiddles (40 KB)
+constexpr uint32_t kMmaTabPart = 8192 + 32768;
+constexpr uint32_t kMmaTabBytes = 2 * kMmaTabPart;
 
 static int brev4(int x) { return ((x & 1) << 3) | ((x & 2) << 1) | ((x & 4) >> 1) | ((x & 8) >> 3); }
 
@@ -76,7 +81,38 @@ void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out) {
   out->assign(kMmaTabBytes, 0);
   uint8_t* t = out->data();
   const uint64_t w16 = h_powmod(omega, 256, p);
-  // row 4 c + r of the B operand: byte r of 2^(8q) w16^(n k), k = col(c)
+  const uint64_t iomega = h_invmod(omega, p), iw16 = h_invmod(w16, p);
+  const uint64_t ninv = h_invmod(4096 % p, p);
+  // row 4 c + r of the B operand: byte r of 2^(8q) r16^(n k) scale, k = col(c),
+  // n = input(K slot)
+  auto bmat_g = [&](uint8_t* dst, uint64_t r16, bool rev_out, bool rev_in, uint64_t scale) {
+    for (int c = 0; c < 16; ++c) {
+      const int k = rev_out ? brev4(c) : c;
+      for (int kn = 0; kn < 16; ++kn) {
+        const int n = rev_in ? brev4(kn) : kn;
+        const uint64_t base = h_mulmod(h_powmod(r16, (uint64_t)n * k, p), scale, p);
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t s = (uint32_t)h_mulmod(base, ((uint64_t)1 << (8 * q)) % p, p);
+          for (int r = 0; r < 4; ++r) {
+            const int row = 4 * c + r, kb = 4 * kn + q;
+            dst[(row >> 3) * 512 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15)] =
+                (uint8_t)(s >> (8 * r));
+          }
+        }
+      }
+    }
+  };
+  auto put = [&](uint8_t* tab, int row, int j, uint64_t w) {
+    const uint32_t pr[2] = {(uint32_t)w, h_shoup((uint32_t)w, p)};
+    memcpy(tab + row * 128 + (((j >> 1) ^ (row & 7)) << 4) + (j & 1) * 8, pr, 8);
+  };
+  bmat_g(t + kMmaTabInv, iw16, false, true, 1);
+  bmat_g(t + kMmaTabInv + 4096, iw16, false, true, ninv);
+  for (int k0 = 0; k0 < 16; ++k0)
+    for (int a = 0; a < 16; ++a)
+      for (int b = 0; b < 16; ++b)
+        put(t + kMmaTabInv + 8192, 16 * k0 + a, b,
+            h_powmod(iomega, (uint64_t)k0 * (a + 16 * b), p));
   auto bmat = [&](uint8_t* dst, bool rev) {
     for (int c = 0; c < 16; ++c) {
       const int k = rev ? brev4(c) : c;
@@ -96,11 +132,7 @@ void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out) {
   bmat(t + kMmaTabB, false);
   bmat(t + kMmaTabBr, true);
   for (int m = 0; m < 256; ++m)
-    for (int j = 0; j < 16; ++j) {
-      const uint64_t w = h_powmod(omega, (uint64_t)m * j, p);
-      const uint32_t pr[2] = {(uint32_t)w, h_shoup((uint32_t)w, p)};
-      memcpy(t + kMmaTabTw + m * 128 + (((j >> 1) ^ (m & 7)) << 4) + (j & 1) * 8, pr, 8);
-    }
+    for (int j = 0; j < 16; ++j) put(t + kMmaTabTw, m, j, h_powmod(omega, (uint64_t)m * j, p));
 }
 
 namespace {
@@ -122,10 +154,11 @@ struct MmaArgs {
   long long in1_stride, in2_stride;  // forward: words between entries' coefficient rows
   uint32_t* out1;
   uint32_t* out2;
-  int n1, n2;                        // entries of the two batches
-  int len;                           // coefficients per entry (<= 4096)
+  long long out_stride;              // inverse: words between entries' outputs
+  int n1, n2;                        // entries of the two batches (inverse: n2 = 0)
+  int len;                           // forward: coefficients per entry; inverse: out_len
   int kc1;                           // K chunks of P1 (2: len <= 2048, else 4)
-  int vec;                           // 16-byte aligned rows (vector loads)
+  int vec;                           // aligned rows: forward 16-byte loads, inverse 32-byte stores
   long long tiles1, tiles;
   uint32_t p, w16s;                  // w16s = floor(2^48 / p): Shoup companion of 2^16
   const uint8_t* tab;
@@ -280,9 +313,49 @@ __device__ __forceinline__ void fwd_store(const MmaArgs& a, uint32_t sdata, int 
   }
 }
 
+// inverse: item = (matrix m = 4j + s, row u, t, K chunk kc): the values at
+// positions 4 kc .. 4 kc + 3 + 16 m + 256 u of entry e0 + t (point-major
+// input in the DIF placement: K slot kappa = bit-reversed k2, matrix m =
+// bit-reversed k1, row u = bit-reversed k0 -- the B matrices and twiddles are
+// indexed accordingly).  The 8 entries of a tile are one 32-byte sector per
+// position.  2048 items per slice.
+struct InvPre {
+  uint32_t v[kInvItems][4];
+};
+__device__ __forceinline__ void inv_load(const TileSrc& s, int j, int w, InvPre& pr) {
+  const int t = w & 7, u = (w >> 3) & 15;
+  const long long e = s.e0 + t;
+  const bool ok = e < s.ne;
+  const uint32_t* base = s.in + (long long)(64 * j + 256 * u) * s.ne + e;
+#pragma unroll
+  for (int r = 0; r < kInvItems; ++r) {
+    const int it = w + kWT * r;
+    const int sm = (it >> 7) & 3, kc = it >> 9;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const long long x = 4 * kc + i + 16 * sm;
+      pr.v[r][i] = ok ? __ldg(base + x * s.ne) : 0u;
+    }
+  }
+}
+__device__ __forceinline__ void inv_store(uint32_t sdata, int j, int w, const InvPre& pr) {
+#pragma unroll
+  for (int r = 0; r < kInvItems; ++r) {
+    const int it = w + kWT * r;
+    const int t = it & 7, u = (it >> 3) & 15, sm = (it >> 7) & 3, kc = it >> 9;
+    sts128(sdata + off_s(4 * j + sm, kc, u * 8 + t), pr.v[r][0], pr.v[r][1], pr.v[r][2],
+           pr.v[r][3]);
+  }
+}
+
+__host__ __device__ constexpr int brev4c(int x) {
+  return ((x & 1) << 3) | ((x & 2) << 1) | ((x & 4) >> 1) | ((x & 8) >> 3);
+}
+
+template <int DIR>  // 0 forward (natural in, DIF PM out), 1 inverse (DIF PM in, natural out)
 __global__ void __launch_bounds__(kThreads, 1)
-    ntt_mma_fwd_kernel(const __grid_constant__ MmaArgs a, const __grid_constant__ CUtensorMap om1,
-                       const __grid_constant__ CUtensorMap om2) {
+    ntt_mma_kernel(const __grid_constant__ MmaArgs a, const __grid_constant__ CUtensorMap om1,
+                   const __grid_constant__ CUtensorMap om2) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = tc::smem_u32(smem);
   const uint32_t sdata = sbase, sB = sbase + kOffB, sTw = sbase + kOffTw, sStage = sbase + kOffStage;
@@ -291,14 +364,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 8;
   uint64_t *staged = bars + 10, *stfree = bars + 11;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  const bool tma_out = a.tma_out;
+  const bool tma_out = DIR == 0 && a.tma_out;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // constant tables: the two B matrices and the twiddles (read once per CTA)
   {
-    const uint4* src = reinterpret_cast<const uint4*>(a.tab);
+    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (DIR ? kMmaTabInv : 0u));
     uint4* dst = reinterpret_cast<uint4*>(smem + kOffB);  // B, B rev, twiddles: contiguous
-    for (int i = tid; i < (int)(kMmaTabBytes / 16); i += kThreads) dst[i] = __ldg(src + i);
+    for (int i = tid; i < (int)(kMmaTabPart / 16); i += kThreads) dst[i] = __ldg(src + i);
   }
   if (tid == 0) {
     tc::mbar_init(&full[0], 1);
@@ -333,8 +406,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {
           const bool lay_k = pass == 1;
-          const int ksteps = pass == 0 ? a.kc1 / 2 : 2;
-          const uint64_t db = dB + (pass == 2 ? (uint64_t)(4096u >> 4) : 0u);  // P3: reversed columns
+          const int ksteps = (DIR == 0 && pass == 0) ? a.kc1 / 2 : 2;
+          // pass 3: forward reversed columns / inverse N^-1 scaled matrix
+          const uint64_t db = dB + (pass == 2 ? (uint64_t)(4096u >> 4) : 0u);
           const uint64_t da = lay_k ? dK : dS;
           const uint32_t lbo = lay_k ? 32768u : 8192u;
 #pragma unroll
@@ -398,13 +472,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sRowR = sdata + (uint32_t)t * 16u;
     const uint32_t sSt = sStage + (uint32_t)(c0 * 128 + u * 8 + t) * 4u;  // [s][c][u][t]
     FwdPre fpre;
+    InvPre ipre;
+    uint32_t yp[4][kVpm];  // inverse: the even chunk's outputs, written with the odd one
     int it = 0;
     long long tile = blockIdx.x;
     if (tile < a.tiles) {
       const TileSrc s0 = tile_src(a, tile);
       for (int j = 0; j < 4; ++j) {
-        fwd_load(a, s0, j, w, fpre);
-        fwd_store(a, sdata, j, w, fpre);
+        if (DIR == 0) {
+          fwd_load(a, s0, j, w, fpre);
+          fwd_store(a, sdata, j, w, fpre);
+        } else {
+          inv_load(s0, j, w, ipre);
+          inv_store(sdata, j, w, ipre);
+        }
         tc::fence_proxy_async();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&ready[j]);
@@ -420,7 +501,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int buf = j & 1;
-          if (pass == 2 && has_next) fwd_load(a, nsrc, j, w, fpre);
+          if (pass == 2 && has_next) {
+            if (DIR == 0)
+              fwd_load(a, nsrc, j, w, fpre);
+            else
+              inv_load(nsrc, j, w, ipre);
+          }
           tc::mbar_wait(&full[buf], (j >> 1) & 1);
           tc::fence_after_sync();
           uint32_t y[4][kVpm];
@@ -444,12 +530,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                           v[ss][4 * i + 3], p, negp, w16s);
           }
           if (pass < 2) {
-            // twiddle w^((u + 16 m) col) in P1 (row digit a = u, MMA digit b),
-            // w^(16 m col) in P2 (MMA digit a)
-            const bool own_row = pass == 0;
+            // forward: w^((u + 16 m) col) in P1 (row digit a = u, MMA digit b),
+            // w^(16 m col) in P2 (MMA digit a); inverse: row 16 k1 (k1 =
+            // brev4(m)), column a in I1; row 16 k0 + u (k0 = brev4(m)),
+            // column b in I2
+            const bool own_row = DIR == 0 ? pass == 0 : pass == 1;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-              const int m = 16 * (4 * j + s) + (own_row ? u : 0);  // m & 7 == (own_row ? u & 7 : 0)
+              const int md = DIR == 0 ? 4 * j + s : brev4c(4 * j + s);
+              const int m = 16 * md + (own_row ? u : 0);  // m & 7 == (own_row ? u & 7 : 0)
               const uint32_t rb = sTw + (uint32_t)m * 128u;
               const int sw = own_row ? (u & 7) : 0;
 #pragma unroll
@@ -462,6 +551,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (pass == 0) {
               // P2 operand: matrix u (= a), row (k0 = c0 + i, t), K chunk j
               const uint32_t mb = off_k(u, j, 0);
+#pragma unroll
+              for (int i = 0; i < kVpm; ++i)
+                sts128(sRow + mb + (uint32_t)i * 128u, y[0][i], y[1][i], y[2][i], y[3][i]);
+            } else if (DIR == 1) {
+              // I3 operand: matrix u (= a), row (b = c0 + i, t), K chunk j
+              const uint32_t mb = off_s(u, j, 0);
 #pragma unroll
               for (int i = 0; i < kVpm; ++i)
                 sts128(sRow + mb + (uint32_t)i * 128u, y[0][i], y[1][i], y[2][i], y[3][i]);
@@ -483,9 +578,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                 x = min(x, x - p);
                 y[s][i] = min(x, x - p);
               }
-            // position c + 16 u + 256 (4 j + s) (= brev12 of the point index)
             const long long e = src.e0 + t;
-            if (tma_out) {
+            if (DIR == 1) {
+              // coefficient a + 16 b + 256 c: a = MMA digit, b = u, c = column.
+              // Chunks are written in pairs: 8 consecutive coefficients per
+              // column from one thread at once
+              if ((j & 1) == 0) {
+#pragma unroll
+                for (int s = 0; s < 4; ++s)
+#pragma unroll
+                  for (int i = 0; i < kVpm; ++i) yp[s][i] = y[s][i];
+              } else if (e < src.ne) {
+                uint32_t* dst = src.out + e * a.out_stride;
+#pragma unroll
+                for (int i = 0; i < kVpm; ++i) {
+                  const int n = 8 * (j >> 1) + 16 * u + 256 * (c0 + i);
+                  if (a.vec && n + 7 < a.len) {
+                    asm volatile(
+                        "st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + n),
+                        "r"(yp[0][i]), "r"(yp[1][i]), "r"(yp[2][i]), "r"(yp[3][i]), "r"(y[0][i]),
+                        "r"(y[1][i]), "r"(y[2][i]), "r"(y[3][i])
+                        : "memory");
+                  } else {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                      if (n + s < a.len) dst[n + s] = yp[s][i];
+#pragma unroll
+                    for (int s = 0; s < 4; ++s)
+                      if (n + 4 + s < a.len) dst[n + 4 + s] = y[s][i];
+                  }
+                }
+              }
+            } else if (tma_out) {
+              // position c + 16 u + 256 (4 j + s) (= brev12 of the point index);
               // staging [s][c][u][t]: one TMA box (8 entries x 1024 positions)
               tc::mbar_wait(stfree, (j & 1) ^ 1);
 #pragma unroll
@@ -509,7 +634,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (has_next) {
               // the last pass's MMAs of chunk j have read slice j: refill it
-              fwd_store(a, sdata, j, w, fpre);
+              if (DIR == 0)
+                fwd_store(a, sdata, j, w, fpre);
+              else
+                inv_store(sdata, j, w, ipre);
               tc::fence_proxy_async();
               __syncwarp();
               if (lane == 0) tc::mbar_arrive(&ready[j]);
@@ -558,24 +686,25 @@ bool out_map(CUtensorMap* m, uint32_t* base, long long ne) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int DIR>
 int launch_mma(MmaArgs a, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma_fwd_kernel,
+    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma_kernel<DIR>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr = true;
   }
   CUtensorMap om1{}, om2{};
   a.tma_out = 0;
-  if (option(kOptNttPmLsu) == 0 && out_map(&om1, a.out1, a.n1) &&
+  if (DIR == 0 && option(kOptNttPmLsu) == 0 && out_map(&om1, a.out1, a.n1) &&
       (a.n2 == 0 || out_map(&om2, a.out2, a.n2)))
     a.tma_out = 1;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = a.tiles < sms ? a.tiles : sms;
-  FPM_CUDA_TRY(launch_pdl(ntt_mma_fwd_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, a,
-                          om1, om2));
+  FPM_CUDA_TRY(launch_pdl(ntt_mma_kernel<DIR>, dim3((unsigned)grid), dim3(kThreads), kSmem, st,
+                          a, om1, om2));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
@@ -584,10 +713,34 @@ bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15) == 0; }
 
 }  // namespace
 
-bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps) {
-  if (logn != 12 || option(kOptNttNoMma) != 0) return false;
+static bool mma_prime_ok(const PrimeSet& ps) {
+  if (option(kOptNttNoMma) != 0) return false;
   if (ps.count != 1 || ps.pr[0].mma == nullptr) return false;
-  if (!(ps.pr[0].p > (1u << 30) && ps.pr[0].p < (1u << 31))) return false;
+  return ps.pr[0].p > (1u << 30) && ps.pr[0].p < (1u << 31);
+}
+
+bool ntt_mma_inv_ok(int logn, const NttInvArgs& a, const PrimeSet& ps) {
+  if (logn != 12 || !mma_prime_ok(ps)) return false;
+  return a.pm && !a.natural && a.off == 0 && a.scale == 1 && a.out_len > 0 && a.out_len <= 4096 &&
+         a.n_entries > 0 && a.n_entries <= (1 << 20);
+}
+
+int launch_ntt_inv_mma(const NttInvArgs& f, const PrimeSet& ps, cudaStream_t st) {
+  MmaArgs a{};
+  a.in1 = f.in; a.out1 = f.out; a.n1 = f.n_entries; a.n2 = 0;
+  a.out_stride = f.out_stride;
+  a.len = f.out_len;
+  a.kc1 = 4;
+  a.vec = (f.out_stride % 8 == 0) && (((uintptr_t)f.out & 31) == 0);
+  a.tiles1 = a.tiles = (a.n1 + 7) / 8;
+  a.p = ps.pr[0].p;
+  a.w16s = (uint32_t)((((uint64_t)1) << 48) / a.p);
+  a.tab = ps.pr[0].mma;
+  return launch_mma<1>(a, st);
+}
+
+bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps) {
+  if (logn != 12 || !mma_prime_ok(ps)) return false;
   // 32-bit point offsets: 4096 * entries < 2^32
   return a.pm && !a.natural && !a.fold && !a.in64 && !a.reduce && a.len > 0 && a.len <= 4096 &&
          a.n_entries <= (1 << 20) && a.n_entries2 <= (1 << 20);
@@ -608,7 +761,7 @@ int launch_ntt_fwd_mma(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t st)
   a.p = ps.pr[0].p;
   a.w16s = (uint32_t)((((uint64_t)1) << 48) / a.p);
   a.tab = ps.pr[0].mma;
-  return launch_mma(a, st);
+  return launch_mma<0>(a, st);
 }
 
 }  // namespace fpm

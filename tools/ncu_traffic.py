@@ -44,11 +44,13 @@ def run(name):
 
 def stage_of(kernel, fwd_seen):
     k = kernel
-    if "ntt_fwd" in k:
+    if "ntt_fwd" in k or "ntt_mma_kernel<0>" in k or "ntt_mma_fwd" in k:
         return "ntt_fwd"
+    if "ntt_mma_kernel<1>" in k:
+        return "ntt_inv"
     if "ntt_inv" in k:
         return "ntt_inv"
-    if "tc_pq" in k or "tc_grouped" in k or "tc_pointwise" in k:
+    if "tc_pq" in k or "tc_grouped" in k or "tc_pointwise" in k or "tc_pair" in k:
         return "pointwise_tc"
     if "pointwise_cc" in k:
         return "pointwise"
