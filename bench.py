@@ -286,10 +286,12 @@ def roofline_report(cfg, cfgname, avg, sbytes):
             "traffic": sum(trs) if all(t is not None for t in trs) else None,
             "algorithmic_bytes": b, "ms": round(ms, 5), "peak_source": hsrc}
     if dom == "ntt":
-        roof["note"] = ("HBM fraction per SURVEY 8(d).  The NTT kernels are bound by the "
-                        "integer multiply path, not HBM: every Shoup modmul issues one IMAD.HI "
-                        "(quarter rate, 4.45 cycles/warp-op/SMSP measured) and two IMAD on the "
-                        "heavy FMA pipe; `compute` gives ncu pipe/issue utilisation, DESIGN.md 4")
+        roof["note"] = ("HBM fraction per SURVEY 8(d).  The NTT kernels are bound by their "
+                        "CUDA-core instruction stream, not HBM: the 4096-point forward runs its "
+                        "radix-16 DFTs on the int8 tensor cores (ntt_mma.cu) and is limited by "
+                        "the limb fold + twiddle epilogue (IMAD.HI at quarter rate); the inverse "
+                        "(Shoup butterflies) by the heavy FMA pipe; `compute` gives ncu "
+                        "pipe/issue utilisation, DESIGN.md 4")
         pipes = read_pipes().get(cfgname, {})
         comp = {}
         for st in ("ntt_fwd", "ntt_inv"):
@@ -300,7 +302,7 @@ def roofline_report(cfg, cfgname, avg, sbytes):
                             "alu_util_elapsed": e["alu_pct_elapsed"],
                             "issue_util_active": e["issue_pct_active"]}
         if comp:
-            roof["compute"] = {"pipe": "fmaheavy (IMAD.HI / IMAD, Shoup butterflies)",
+            roof["compute"] = {"pipe": "fmaheavy (IMAD.HI / IMAD: Shoup twiddles, limb folds)",
                                "per_kernel": comp,
                                "int_rates_cycles_per_warp_op": INT_RATES,
                                "source": "profiles/ncu_pipes.json (ncu --set full), "

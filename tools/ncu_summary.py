@@ -33,9 +33,19 @@ METRICS = [
     "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "smsp__issue_active.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "smsp__pcsamp_warps_issue_stalled_long_scoreboard",
+    "smsp__pcsamp_warps_issue_stalled_wait",
+    "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle",
+    "smsp__pcsamp_warps_issue_stalled_selected",
+    "smsp__pcsamp_warps_issue_stalled_not_selected",
+    "smsp__pcsamp_warps_issue_stalled_barrier",
+    "smsp__pcsamp_warps_issue_stalled_mio_throttle",
+    "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
 ]
 
-STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_inv": "ntt_inv", "pointwise_cc": "pointwise",
+STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_mma_kernel<0>": "ntt_fwd", "ntt_mma_kernel<1>": "ntt_inv",
+            "ntt_inv": "ntt_inv", "pointwise_cc": "pointwise", "tc_pair": "pointwise_tc",
             "tc_pointwise": "pointwise_tc", "tc_grouped": "pointwise_tc", "tc_pq": "pointwise_tc",
             "crt_kernel": "crt"}
 
