@@ -36,7 +36,9 @@
 // holding 4 consecutive MMAs of a chunk emits one 16-byte K chunk per
 // output column (conflict-free: the 8 lanes of a quarter warp are the 8
 // transforms of one row group).  Any residue < 2^32 is a valid operand, so
-// values are only reduced below p at the output.
+// values are only reduced below p by the inverse's output (the forward's
+// evaluations feed only the int8 tensor-core products, which take any
+// 32-bit residue).
 //
 // Shared memory (one persistent CTA per SM): a 128 KB data region holding
 // the tile's operands in place -- alternately "slice-major" (matrix m in
@@ -570,14 +572,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           } else {
+            // forward evaluations stay unreduced (< 2^31 + p): their only
+            // consumers are the int8 tensor-core products, whose limb
+            // identity takes any 32-bit residue (tc_pair.cu, tc_grouped.cu);
+            // the inverse's coefficients are reduced below p
+            if (DIR == 1) {
 #pragma unroll
-            for (int s = 0; s < 4; ++s)
+              for (int s = 0; s < 4; ++s)
 #pragma unroll
-              for (int i = 0; i < kVpm; ++i) {
-                uint32_t x = y[s][i];
-                x = min(x, x - p);
-                y[s][i] = min(x, x - p);
-              }
+                for (int i = 0; i < kVpm; ++i) {
+                  uint32_t x = y[s][i];
+                  x = min(x, x - p);
+                  y[s][i] = min(x, x - p);
+                }
+            }
             const long long e = src.e0 + t;
             if (DIR == 1) {
               // coefficient a + 16 b + 256 c: a = MMA digit, b = u, c = column.
