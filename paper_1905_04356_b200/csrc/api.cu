@@ -415,10 +415,10 @@ int fpm_polmat_mul_host(fpm_context* ctx, uint64_t p, int elem_bytes, const void
   FPM_TRY(ws.get(esz * nb + 1, &dB));
   FPM_TRY(ws.get(esz * nc + 1, &dC));
   const int force = (int)option(kOptHostBlocks);
-  // block count by output size (cfg5, 1 GB of C: R = 8 28.6 ms, 4 29.4, 6 35.3,
+  // block count by output size (cfg5, 1.07 GB of C: R = 8 28.6 ms, 4 29.4, 6 35.3,
   // 2 32.6 -- the first block's inputs are the pipeline fill)
   int R = force > 0 ? force
-                    : (esz * nc >= (1ull << 30) ? 8
+                    : (esz * nc >= (1ull << 29) ? 8
                        : esz * nc >= (256u << 20) ? 4 : esz * nc >= (8u << 20) ? 3 : 1);
   if (R > m) R = m;
   if (R > n) R = n;
