@@ -416,13 +416,19 @@ int polmat_middle(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRef
   A.len = da + 1;
   B.len = db + 1;
   if (exact) {
-    // true slice: cyclic length covering the whole product, window at c
+    // true slice: a cyclic length N with c + w <= N (the window fits) and
+    // plen - N <= c (product coefficients >= N alias below c, never into the
+    // window); A must fit (da < N), B longer than N is folded.  At the PM-Basis
+    // nodes (da ~ c, db ~ 2c) this is half the full-product length.
     if (c > da + db) return zero_out(C, ec, 0, C.len, st);
     const long long plen = (long long)da + db + 1;
-    const int logn = ceil_log2_min1(plen);
     OutRef C2 = C;
     long long w = d < C.len ? d : C.len;
     if (w > plen - c) w = plen - c;  // positions past the product are zero
+    long long need = c + w;
+    if (plen - c > need) need = plen - c;
+    if (da + 1 > need) need = da + 1;
+    const int logn = ceil_log2_min1(need);
     C2.len = (int)w;
     FPM_TRY(cyclic_product(cx, p, m, k, n, A, B, logn, c, C2));
     return zero_out(C, ec, C2.len, C.len, st);
