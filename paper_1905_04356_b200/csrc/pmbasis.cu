@@ -396,6 +396,10 @@ int pmbasis_rec(Context& cx, uint64_t p, int is64, const void* F, int m, int n, 
   return kOk;
 }
 
+// nodes of this order and above size their products from P1's / P2's actual
+// degrees (two host synchronisations per node: 7 nodes at cfg4's sigma 4096)
+constexpr int kSizedNode = 1024;
+
 // Sync-free recursion for 31-bit primes with shared-memory leaves: the
 // shift stays on the device (each leaf turns s into s + delta, which equals
 // rdeg_s of its basis, and composing leaves composes the shifts), and all
@@ -414,17 +418,33 @@ int pmbasis_rec_dev(Context& cx, uint32_t p, const void* F, int m, int n, long l
   FPM_TRY(ws.get((size_t)m * m * (o1 + 1), &P1));
   FPM_TRY(ws.get((size_t)m, &s1));
   FPM_TRY(pmbasis_rec_dev(cx, p, F, m, n, fs, lf < o1 ? lf : o1, o1, s_dev, T, P1, o1 + 1, s1));
+  // large nodes read the actual degree of P1 back (one host synchronisation):
+  // generic bases have degree ~ order n / m, and the product below then runs
+  // at half the transform length of the a-priori bound deg P <= order
+  const bool sized = order >= kSizedNode;
+  int lp1 = o1 + 1;
+  if (sized) {
+    int dg = -1;
+    FPM_TRY(matrix_degree(cx, P1, 0, (long long)m * m, o1 + 1, &dg));
+    lp1 = dg + 1 > 0 ? dg + 1 : 1;
+  }
   FPM_TRY(ws.get((size_t)m * n * (o2 > 0 ? o2 : 1), &R));
   {
-    MatRef A{P1, 0, o1 + 1, o1 + 1};
+    MatRef A{P1, 0, o1 + 1, lp1};
     MatRef B{F, 0, fs, lt};
     OutRef Ro{R, 0, o2, o2};
-    FPM_TRY(polmat_middle(cx, p, m, m, n, A, B, o1, lt - 1, o1, o2, 1, Ro));
+    FPM_TRY(polmat_middle(cx, p, m, m, n, A, B, lp1 - 1, lt - 1, o1, o2, 1, Ro));
   }
   FPM_TRY(ws.get((size_t)m * m * (o2 + 1), &P2));
   FPM_TRY(pmbasis_rec_dev(cx, p, R, m, n, o2, o2, o2, s1, T, P2, o2 + 1, sft_dev));
-  MatRef A2{P2, 0, o2 + 1, o2 + 1};
-  MatRef B2{P1, 0, o1 + 1, o1 + 1};
+  int lp2 = o2 + 1;
+  if (sized) {
+    int dg = -1;
+    FPM_TRY(matrix_degree(cx, P2, 0, (long long)m * m, o2 + 1, &dg));
+    lp2 = dg + 1 > 0 ? dg + 1 : 1;
+  }
+  MatRef A2{P2, 0, o2 + 1, lp2};
+  MatRef B2{P1, 0, o1 + 1, lp1};
   OutRef Co{P, 0, ps, (int)ps};
   return polmat_mul(cx, p, m, m, m, A2, B2, Co);
 }
