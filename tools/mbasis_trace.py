@@ -18,7 +18,7 @@ from paper_1905_04356_b200 import _lib, dense  # noqa: E402
 def main():
     cfg = dict(bench.CONFIGS["cfg4"], sigma=256)
     F = bench.make_inputs(cfg, "cuda", 4)[0]
-    dense.pmbasis_dense(F, cfg["sigma"], [0] * cfg["m"], cfg["p"], T=16)
+    dense.pmbasis_dense(F, cfg["sigma"], [0] * cfg["m"], cfg["p"], T=int(os.environ.get("LEAF_T", "16")))
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * 512)()
     assert _lib.lib().fpm_debug_mbasis_trace(buf) == 0
