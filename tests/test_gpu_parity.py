@@ -169,15 +169,28 @@ def test_host_abi_matches_device():
     _ = ctypes
 
 
-@pytest.mark.parametrize("p,m,k,n,la,lb", [
-    (P31, 9, 3, 11, 16000, 16000),   # C >= 8 MB: 4 x 4 pipelined blocks, uneven edges
-    (P60, 8, 2, 9, 9000, 9000),      # u64 CRT path through the same pipeline
+@pytest.mark.parametrize("p,m,k,n,la,lb,blocks", [
+    (P31, 9, 3, 11, 16000, 16000, 0),   # C >= 8 MB: 4 x 4 pipelined blocks, uneven edges
+    (P60, 8, 2, 9, 9000, 9000, 0),      # u64 CRT path through the same pipeline
+    (P31, 64, 48, 72, 2048, 2048, 8),   # 8 x 8 blocks (the >= 512 MB rule), tensor-core NTT
+    (P31, 200, 40, 136, 1500, 600, 2),  # 2 x 2: 100-row blocks on tc_grouped, 68-column B blocks
 ])
-def test_host_abi_pipelined_blocks(p, m, k, n, la, lb):
+def test_host_abi_pipelined_blocks(p, m, k, n, la, lb, blocks):
     """fpm_polmat_mul_host on a product large enough for the block pipeline
     (copy-in / compute / copy-out streams) equals the device entry point."""
     import torch
 
+    from paper_1905_04356_b200 import _lib
+
+    _lib.set_option("host_blocks", blocks)
+    try:
+        _host_blocks_case(p, m, k, n, la, lb)
+    finally:
+        _lib.set_option("host_blocks", 0)
+    _ = torch
+
+
+def _host_blocks_case(p, m, k, n, la, lb):
     from paper_1905_04356_b200 import _lib
 
     eb = dense.elem_bytes_for(p)
@@ -195,7 +208,6 @@ def test_host_abi_pipelined_blocks(p, m, k, n, la, lb):
     for (i, j) in [(0, 0), (m - 1, n - 1), (m // 2, n // 3)]:
         exp = O.pm_mul(p, A[i:i + 1], B[:, j:j + 1])
         assert np.array_equal(Ch[i, j].astype(np.uint64), exp[0, 0])
-    _ = torch
 
 
 def _sha_of_mul(seed, p, m, k, n, deg):
