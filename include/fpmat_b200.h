@@ -27,8 +27,10 @@
  *     except where the reference's own dispatch needs a device value on the
  *     host: fpm_polmat_middle / fpm_pm_middle_product read deg A and deg B
  *     (one synchronisation, polmat.py:477-497) and fpm_mbasis / fpm_pmbasis
- *     return *lp = deg P + 1 (one synchronisation at exit).  *_host entry
- *     points return after their results are in host memory.
+ *     return *lp = deg P + 1 (one synchronisation at exit; fpm_pmbasis also
+ *     reads back the degrees of the two child bases at every node of order
+ *     >= 1024 to size that node's product).  *_host entry points return
+ *     after their results are in host memory.
  */
 #ifndef FPMAT_B200_H
 #define FPMAT_B200_H
