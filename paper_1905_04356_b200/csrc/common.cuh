@@ -155,7 +155,6 @@ enum Option : int {
   kOptNttNoMma,           // "ntt_no_mma": no tensor-core NTT (ntt_mma.cu)
   kOptTcNoPair,           // "tc_no_pair": tc_grouped instead of tc_pair for 128 < m <= 256
   kOptTcPair1,            // "tc_pair1": one-SM tc_pair instead of the CTA-pair kernel
-  kOptNttMmaInv,          // "ntt_mma_inv": tensor-core inverse (measured slower; A/B only)
   kOptCount
 };
 long long option(Option o);

@@ -421,9 +421,6 @@ int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStr
 
 int launch_ntt_inv(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
   if (a.n_entries <= 0) return kOk;
-  // tensor-core inverse: opt-in (cfg5 1.29 ms with 32-byte aligned output rows,
-  // 2.03 ms with 4095-word rows, against 1.03 ms for the Shoup kernel below)
-  if (option(kOptNttMmaInv) != 0 && ntt_mma_inv_ok(logn, a, ps)) return launch_ntt_inv_mma(a, ps, st);
   const bool no_persist = option(kOptNttGeneric) != 0;
   if (!no_persist && ntt_tma_inv_ok(logn, a)) return launch_ntt_inv_tma(logn, a, ps, st);
   if (!no_persist && ntt_persist_inv_ok(logn, a)) return launch_ntt_inv_persist(logn, a, ps, st);

@@ -35,23 +35,32 @@
 // operand: the next pass's K digit is this pass's MMA digit, so a thread
 // holding 4 consecutive MMAs of a chunk emits one 16-byte K chunk per
 // output column (conflict-free: the 8 lanes of a quarter warp are the 8
-// transforms of one row group).  Any residue < 2^32 is a valid operand, so
-// values are only reduced below p by the inverse's output (the forward's
-// evaluations feed only the int8 tensor-core products, which take any
-// 32-bit residue).
+// transforms of one row group).  Any residue < 2^32 is a valid operand, and
+// the evaluations feed only the int8 tensor-core products, which take any
+// 32-bit residue: nothing is reduced below p.
 //
 // Shared memory (one persistent CTA per SM): a 128 KB data region holding
 // the tile's operands in place -- alternately "slice-major" (matrix m in
 // slice m/4) and "chunk-major" (K chunk kc of every matrix in slice kc), so
 // that chunk j of a pass only overwrites what the MMAs of chunk j have read
-// -- the B matrices and the twiddle table.  TMEM: two 256-column buffers
-// (4 MMAs x 64 columns each), so the MMAs of chunk j+1 overlap the
-// epilogue of chunk j.  Warp 0 issues the MMAs (one thread); warps 1..16
-// are the workers: TMEM lane quarter warp % 4, column quarter (warp-1) / 4.
-// Outputs go through a 32 KB staging tile, one TMA box per chunk (8
-// entries x 1024 positions, 32-byte point rows), issued by warp 17.  The next tile's input is
-// loaded into registers during the last pass and stored into slice j as soon
-// as the last pass's MMAs of chunk j are done.
+// -- the B matrices, the twiddle table and a 32 KB output staging tile.
+// TMEM: two 256-column buffers (4 MMAs x 64 columns each), so the MMAs of
+// chunk j+1 overlap the epilogue of chunk j.  Roles: warp 0 issues the MMAs
+// (one thread); warps 1..16 are the workers (TMEM lane quarter warp % 4,
+// column quarter (warp-1) / 4); warp 17 issues the TMA stores of the outputs
+// (one box of 8 entries x 1024 positions, 32-byte point rows, per chunk of
+// the last pass) and prefetches the next tile's input rows into L2; warps
+// 18..19 load the next tile's input (L2 hits) and store slice j as soon as
+// the last pass's MMAs of chunk j are done.
+//
+// Measured on cfg5 (timeline of clock64 stamps per chunk, profiles/r02):
+// P1 / P2 chunks ~1.1-1.5 K cycles, P3 chunks bound by the TMA store of the
+// 32-byte point rows (~1.5-2 K cycles per 32 KB box); the L2 prefetch of the
+// next tile's input took the kernel 1.58 -> 1.38 ms, the input warps 1.38 ->
+// 1.33 ms.  Rejected (slower): two 8-warp worker groups on alternating
+// chunks (1.47), per-MMA TMEM-slot release (1.73), out-of-order MMA issue per
+// group (2.12), staging in the freed data slices (1.46), half-chunk ping-pong
+// staging (1.34-1.37: the TMA store rate, not the wait, bounds P3).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <vector>
@@ -67,57 +76,20 @@ namespace fpm {
 //   [0, 4K)      DFT16 B operand (K-major SWIZZLE_NONE, LBO 128, SBO 512)
 //   [4K, 8K)     the same with bit-reversed output columns (pass 3)
 //   [8K, 40K)    twiddles: row m < 256, column j < 16: w^(m j)
-//   [40K, 44K)   inverse DFT16 B operand, K rows in bit-reversed input order
-//   [44K, 48K)   the same times N^-1 (inverse pass 3)
-//   [48K, 80K)   inverse twiddles: row 16 k0 + a, column b: w^-(k0 (a + 16 b))
 // twiddle rows hold 16 (w, floor(w 2^32 / p)) pairs = 128 bytes; the 16-byte
 // chunk c of row m is stored at chunk c ^ (m & 7) (conflict-free row reads).
 constexpr uint32_t kMmaTabB = 0, kMmaTabBr = 4096, kMmaTabTw = 8192;
-constexpr uint32_t kMmaTabInv = 40960;  // inverse tables: B, B N^-1, twiddles (40 KB)
-constexpr uint32_t kMmaTabPart = 8192 + 32768;
-constexpr uint32_t kMmaTabBytes = 2 * kMmaTabPart;
-
-static int brev4(int x) { return ((x & 1) << 3) | ((x & 2) << 1) | ((x & 4) >> 1) | ((x & 8) >> 3); }
+constexpr uint32_t kMmaTabBytes = 8192 + 32768;
 
 void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out) {
   out->assign(kMmaTabBytes, 0);
   uint8_t* t = out->data();
   const uint64_t w16 = h_powmod(omega, 256, p);
-  const uint64_t iomega = h_invmod(omega, p), iw16 = h_invmod(w16, p);
-  const uint64_t ninv = h_invmod(4096 % p, p);
-  // row 4 c + r of the B operand: byte r of 2^(8q) r16^(n k) scale, k = col(c),
-  // n = input(K slot)
-  auto bmat_g = [&](uint8_t* dst, uint64_t r16, bool rev_out, bool rev_in, uint64_t scale) {
-    for (int c = 0; c < 16; ++c) {
-      const int k = rev_out ? brev4(c) : c;
-      for (int kn = 0; kn < 16; ++kn) {
-        const int n = rev_in ? brev4(kn) : kn;
-        const uint64_t base = h_mulmod(h_powmod(r16, (uint64_t)n * k, p), scale, p);
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t s = (uint32_t)h_mulmod(base, ((uint64_t)1 << (8 * q)) % p, p);
-          for (int r = 0; r < 4; ++r) {
-            const int row = 4 * c + r, kb = 4 * kn + q;
-            dst[(row >> 3) * 512 + (kb >> 4) * 128 + (row & 7) * 16 + (kb & 15)] =
-                (uint8_t)(s >> (8 * r));
-          }
-        }
-      }
-    }
-  };
-  auto put = [&](uint8_t* tab, int row, int j, uint64_t w) {
-    const uint32_t pr[2] = {(uint32_t)w, h_shoup((uint32_t)w, p)};
-    memcpy(tab + row * 128 + (((j >> 1) ^ (row & 7)) << 4) + (j & 1) * 8, pr, 8);
-  };
-  bmat_g(t + kMmaTabInv, iw16, false, true, 1);
-  bmat_g(t + kMmaTabInv + 4096, iw16, false, true, ninv);
-  for (int k0 = 0; k0 < 16; ++k0)
-    for (int a = 0; a < 16; ++a)
-      for (int b = 0; b < 16; ++b)
-        put(t + kMmaTabInv + 8192, 16 * k0 + a, b,
-            h_powmod(iomega, (uint64_t)k0 * (a + 16 * b), p));
+  // row 4 c + r of the B operand: byte r of 2^(8q) w16^(n k), k = col(c), n =
+  // the K slot's input digit
   auto bmat = [&](uint8_t* dst, bool rev) {
     for (int c = 0; c < 16; ++c) {
-      const int k = rev ? brev4(c) : c;
+      const int k = rev ? ((c & 1) << 3) | ((c & 2) << 1) | ((c & 4) >> 1) | ((c & 8) >> 3) : c;
       for (int n = 0; n < 16; ++n) {
         const uint64_t base = h_powmod(w16, (uint64_t)n * k, p);
         for (int q = 0; q < 4; ++q) {
@@ -134,33 +106,37 @@ void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out) {
   bmat(t + kMmaTabB, false);
   bmat(t + kMmaTabBr, true);
   for (int m = 0; m < 256; ++m)
-    for (int j = 0; j < 16; ++j) put(t + kMmaTabTw, m, j, h_powmod(omega, (uint64_t)m * j, p));
+    for (int j = 0; j < 16; ++j) {
+      const uint64_t w = h_powmod(omega, (uint64_t)m * j, p);
+      const uint32_t pr[2] = {(uint32_t)w, h_shoup((uint32_t)w, p)};
+      memcpy(t + kMmaTabTw + m * 128 + (((j >> 1) ^ (m & 7)) << 4) + (j & 1) * 8, pr, 8);
+    }
 }
 
 namespace {
 
-constexpr int kWorkers = 16;                    // worker warps (4 per TMEM lane quarter)
-constexpr int kParts = kWorkers / 4;            // column parts per lane quarter
-constexpr int kVpm = 16 / kParts;               // outputs of one MMA per worker thread
-constexpr int kThreads = 32 * (2 + kWorkers);   // + the MMA warp + the store warp
-constexpr uint32_t kData = 131072;              // 8 transforms x 4096 words
-constexpr uint32_t kOffB = kData;               // B matrices (natural, reversed columns)
+constexpr int kWorkers = 16;                     // worker warps (warps 1 .. 16)
+constexpr int kLoaders = 2;                      // input warps (after the store warp)
+constexpr int kVpm = 4;                          // outputs of one MMA per worker thread
+constexpr int kThreads = 32 * (2 + kWorkers + kLoaders);
+constexpr int kLT = 32 * kLoaders;               // loader threads
+constexpr uint32_t kData = 131072;               // 8 transforms x 4096 words
+constexpr uint32_t kOffB = kData;                // B matrices (natural, reversed columns)
 constexpr uint32_t kOffTw = kOffB + 8192;
-constexpr uint32_t kOffStage = kOffTw + 32768;  // output staging (one TMA box)
+constexpr uint32_t kOffStage = kOffTw + 32768;   // output staging (one TMA box)
 constexpr uint32_t kOffBar = kOffStage + 32768;
-constexpr size_t kSmem = kOffBar + 128;
+constexpr size_t kSmem = kOffBar + 256;
 
 struct MmaArgs {
   const uint32_t* in1;
   const uint32_t* in2;
-  long long in1_stride, in2_stride;  // forward: words between entries' coefficient rows
+  long long in1_stride, in2_stride;  // words between entries' coefficient rows
   uint32_t* out1;
   uint32_t* out2;
-  long long out_stride;              // inverse: words between entries' outputs
-  int n1, n2;                        // entries of the two batches (inverse: n2 = 0)
-  int len;                           // forward: coefficients per entry; inverse: out_len
+  int n1, n2;                        // entries of the two batches
+  int len;                           // coefficients per entry
   int kc1;                           // K chunks of P1 (2: len <= 2048, else 4)
-  int vec;                           // aligned rows: forward 16-byte loads, inverse 32-byte stores
+  int vec;                           // 16-byte aligned rows: vector loads
   long long tiles1, tiles;
   uint32_t p, w16s;                  // w16s = floor(2^48 / p): Shoup companion of 2^16
   const uint8_t* tab;
@@ -221,11 +197,6 @@ __device__ __forceinline__ uint32_t prmt0(uint32_t a, uint32_t sel) {
   return r;
 }
 
-__device__ __forceinline__ void tmem_ldv(uint32_t taddr, uint32_t (&v)[16]) { tmem_ld16_nw(taddr, v); }
-__device__ __forceinline__ void tmem_ldv(uint32_t taddr, uint32_t (&v)[32]) {
-  tc::tmem_ld32_nw(taddr, v);
-}
-
 // sum_r 2^(8r) d[r] (d[r] < 2^22) -> a congruent word < 2^31 + p:
 // H = d2 + 2^8 d3 < 2^31, H 2^16 mod p by Shoup (q = hi(H w16s)), then
 // d0 + 2^8 d1 + (H 2^16 mod p).  negp = 2^32 - p.
@@ -246,37 +217,33 @@ __device__ __forceinline__ uint32_t shoup_n(uint32_t a, uint32_t w, uint32_t ws,
 struct TileSrc {
   const uint32_t* in;
   long long stride;
-  uint32_t* out;
   int ne;
   long long e0;
 };
 __device__ __forceinline__ TileSrc tile_src(const MmaArgs& a, long long tile) {
   TileSrc s;
   if (tile < a.tiles1) {
-    s.in = a.in1; s.stride = a.in1_stride; s.out = a.out1; s.ne = a.n1; s.e0 = tile * 8;
+    s.in = a.in1; s.stride = a.in1_stride; s.ne = a.n1; s.e0 = tile * 8;
   } else {
-    s.in = a.in2; s.stride = a.in2_stride; s.out = a.out2; s.ne = a.n2;
-    s.e0 = (tile - a.tiles1) * 8;
+    s.in = a.in2; s.stride = a.in2_stride; s.ne = a.n2; s.e0 = (tile - a.tiles1) * 8;
   }
   return s;
 }
 
-// ---- input of one slice (P1 / I1 operand, slice-major) ------------------------
-// forward: item = (matrix b = 4j + s, a-quad, t, K chunk): four 16-byte loads
-// x[4aq .. 4aq+3 + 16 b + 256 c], c = 4 kc .. 4 kc + 3, transposed into four
-// 16-byte K chunks of rows (a, t).  Up to 512 items = one per worker thread.
-constexpr int kWT = 32 * kWorkers;                 // worker threads
-constexpr int kFwdItems = (512 + kWT - 1) / kWT;     // forward items per thread (K' = 64)
-constexpr int kInvItems = 2048 / kWT;                // inverse items per thread
-struct FwdPre {
-  uint4 g[kFwdItems][4];
+// ---- input of one slice (P1 operand, slice-major) -----------------------------
+// item = (transform t, a-quad aq, matrix b = 4j + sm, K chunk kc): four
+// 16-byte loads x[4aq .. 4aq+3 + 16 b + 256 c], c = 4 kc .. 4 kc + 3,
+// transposed into four 16-byte K chunks of rows (a, t).  128 kc1 items per
+// slice, kLT * kLoadItems per round.
+constexpr int kLoadItems = 4;
+struct LoadBuf {
+  uint4 g[kLoadItems][4];
 };
-__device__ __forceinline__ void fwd_load(const MmaArgs& a, const TileSrc& s, int j, int w,
-                                         FwdPre& pr) {
+__device__ __forceinline__ void slice_load(const MmaArgs& a, const TileSrc& s, int j, int i0,
+                                           LoadBuf& lb) {
 #pragma unroll
-  for (int r = 0; r < kFwdItems; ++r) {
-    const int it = w + kWT * r;
-    if (it >= 128 * a.kc1) break;
+  for (int r = 0; r < kLoadItems; ++r) {
+    const int it = i0 + kLT * r;
     const int t = it & 7, aq = (it >> 3) & 3, sm = (it >> 5) & 3, kc = it >> 7;
     const long long e = s.e0 + t;
     const int b = 4 * j + sm;
@@ -295,19 +262,17 @@ __device__ __forceinline__ void fwd_load(const MmaArgs& a, const TileSrc& s, int
           if (n + 3 < a.len) v.w = __ldg(src + 3);
         }
       }
-      pr.g[r][i] = v;
+      lb.g[r][i] = v;
     }
   }
 }
-__device__ __forceinline__ void fwd_store(const MmaArgs& a, uint32_t sdata, int j, int w,
-                                          const FwdPre& pr) {
+__device__ __forceinline__ void slice_store(uint32_t sdata, int j, int i0, const LoadBuf& lb) {
 #pragma unroll
-  for (int r = 0; r < kFwdItems; ++r) {
-    const int it = w + kWT * r;
-    if (it >= 128 * a.kc1) break;
+  for (int r = 0; r < kLoadItems; ++r) {
+    const int it = i0 + kLT * r;
     const int t = it & 7, aq = (it >> 3) & 3, sm = (it >> 5) & 3, kc = it >> 7;
     const int b = 4 * j + sm;
-    const uint4* g = pr.g[r];
+    const uint4* g = lb.g[r];
     sts128(sdata + off_s(b, kc, (4 * aq + 0) * 8 + t), g[0].x, g[1].x, g[2].x, g[3].x);
     sts128(sdata + off_s(b, kc, (4 * aq + 1) * 8 + t), g[0].y, g[1].y, g[2].y, g[3].y);
     sts128(sdata + off_s(b, kc, (4 * aq + 2) * 8 + t), g[0].z, g[1].z, g[2].z, g[3].z);
@@ -315,46 +280,6 @@ __device__ __forceinline__ void fwd_store(const MmaArgs& a, uint32_t sdata, int 
   }
 }
 
-// inverse: item = (matrix m = 4j + s, row u, t, K chunk kc): the values at
-// positions 4 kc .. 4 kc + 3 + 16 m + 256 u of entry e0 + t (point-major
-// input in the DIF placement: K slot kappa = bit-reversed k2, matrix m =
-// bit-reversed k1, row u = bit-reversed k0 -- the B matrices and twiddles are
-// indexed accordingly).  The 8 entries of a tile are one 32-byte sector per
-// position.  2048 items per slice.
-struct InvPre {
-  uint32_t v[kInvItems][4];
-};
-__device__ __forceinline__ void inv_load(const TileSrc& s, int j, int w, InvPre& pr) {
-  const int t = w & 7, u = (w >> 3) & 15;
-  const long long e = s.e0 + t;
-  const bool ok = e < s.ne;
-  const uint32_t* base = s.in + (long long)(64 * j + 256 * u) * s.ne + e;
-#pragma unroll
-  for (int r = 0; r < kInvItems; ++r) {
-    const int it = w + kWT * r;
-    const int sm = (it >> 7) & 3, kc = it >> 9;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const long long x = 4 * kc + i + 16 * sm;
-      pr.v[r][i] = ok ? __ldg(base + x * s.ne) : 0u;
-    }
-  }
-}
-__device__ __forceinline__ void inv_store(uint32_t sdata, int j, int w, const InvPre& pr) {
-#pragma unroll
-  for (int r = 0; r < kInvItems; ++r) {
-    const int it = w + kWT * r;
-    const int t = it & 7, u = (it >> 3) & 15, sm = (it >> 7) & 3, kc = it >> 9;
-    sts128(sdata + off_s(4 * j + sm, kc, u * 8 + t), pr.v[r][0], pr.v[r][1], pr.v[r][2],
-           pr.v[r][3]);
-  }
-}
-
-__host__ __device__ constexpr int brev4c(int x) {
-  return ((x & 1) << 3) | ((x & 2) << 1) | ((x & 4) >> 1) | ((x & 8) >> 3);
-}
-
-template <int DIR>  // 0 forward (natural in, DIF PM out), 1 inverse (DIF PM in, natural out)
 __global__ void __launch_bounds__(kThreads, 1)
     ntt_mma_kernel(const __grid_constant__ MmaArgs a, const __grid_constant__ CUtensorMap om1,
                    const __grid_constant__ CUtensorMap om2) {
@@ -362,27 +287,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = tc::smem_u32(smem);
   const uint32_t sdata = sbase, sB = sbase + kOffB, sTw = sbase + kOffTw, sStage = sbase + kOffStage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  // full[2], empty[2], slice ready[4], pass done[2], staged, stage free; TMEM base
-  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 8;
-  uint64_t *staged = bars + 10, *stfree = bars + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
-  const bool tma_out = DIR == 0 && a.tma_out;
+  // full[2], empty[2], slice ready[4], last-pass chunk done[4], pass done[2],
+  // staged, stage free; TMEM base
+  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *p3done = bars + 8;
+  uint64_t *pdone = bars + 12, *staged = bars + 14, *stfree = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   // constant tables: the two B matrices and the twiddles (read once per CTA)
   {
-    const uint4* src = reinterpret_cast<const uint4*>(a.tab + (DIR ? kMmaTabInv : 0u));
+    const uint4* src = reinterpret_cast<const uint4*>(a.tab);
     uint4* dst = reinterpret_cast<uint4*>(smem + kOffB);  // B, B rev, twiddles: contiguous
-    for (int i = tid; i < (int)(kMmaTabPart / 16); i += kThreads) dst[i] = __ldg(src + i);
+    for (int i = tid; i < (int)(kMmaTabBytes / 16); i += kThreads) dst[i] = __ldg(src + i);
   }
   if (tid == 0) {
-    tc::mbar_init(&full[0], 1);
-    tc::mbar_init(&full[1], 1);
-    tc::mbar_init(&empty[0], kWorkers);
-    tc::mbar_init(&empty[1], kWorkers);
-    for (int j = 0; j < 4; ++j) tc::mbar_init(&ready[j], kWorkers);
-    tc::mbar_init(&pdone[0], kWorkers);
-    tc::mbar_init(&pdone[1], kWorkers);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&full[b], 1);
+      tc::mbar_init(&empty[b], kWorkers);
+      tc::mbar_init(&pdone[b], kWorkers);
+    }
+    for (int j = 0; j < 4; ++j) {
+      tc::mbar_init(&ready[j], kLoaders);
+      tc::mbar_init(&p3done[j], 1);
+    }
     tc::mbar_init(staged, kWorkers);
     tc::mbar_init(stfree, 1);
     tc::fence_mbar_init();
@@ -408,16 +335,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int pass = 0; pass < 3; ++pass) {
           const bool lay_k = pass == 1;
-          const int ksteps = (DIR == 0 && pass == 0) ? a.kc1 / 2 : 2;
-          // pass 3: forward reversed columns / inverse N^-1 scaled matrix
-          const uint64_t db = dB + (pass == 2 ? (uint64_t)(4096u >> 4) : 0u);
+          const int ksteps = pass == 0 ? a.kc1 / 2 : 2;
+          const uint64_t db = dB + (pass == 2 ? (uint64_t)(4096u >> 4) : 0u);  // reversed columns
           const uint64_t da = lay_k ? dK : dS;
           const uint32_t lbo = lay_k ? 32768u : 8192u;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            // 12 chunks per tile: buffer j & 1, its (j >> 1)-th use in this pass
+            // buffer j & 1, its (j >> 1)-th use in this pass; the MMA thread
+            // polls (test_wait): it must react at once
             const int buf = j & 1;
-            // the MMA thread polls (test_wait): it must react at once
             tc::mbar_wait_spin(tc::smem_u32(&empty[buf]), ((j >> 1) & 1) ^ 1);
             if (pass == 0)
               tc::mbar_wait_spin(tc::smem_u32(&ready[j]), it & 1);
@@ -434,18 +360,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc::mma_u8(d, da + ((a0 + 2 * lbo) >> 4), db + (256 >> 4), idesc, 1u);
             }
             tc::commit(&full[buf]);
+            if (pass == 2) tc::commit(&p3done[j]);  // slice j may be refilled
           }
         }
       }
     }
   } else if (warp == kWorkers + 1) {
     // ------------------------- output store warp (TMA) -------------------------
-    if (tma_out && lane == 0) {
+    if (a.tma_out && lane == 0) {
       tc::prefetch_tmap(&om1);
       tc::prefetch_tmap(&om2);
       for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
         const bool second = tile >= a.tiles1;
         const int e0 = (int)((second ? tile - a.tiles1 : tile) * 8);
+        // the next tile's input rows into L2 a tile ahead, so that the input
+        // warps see L2 latency, not DRAM's (-12 % kernel time on cfg5)
+        if (a.vec && tile + gridDim.x < a.tiles) {
+          const TileSrc ns = tile_src(a, tile + gridDim.x);
+          const uint32_t bytes = (uint32_t)((a.len * 4 + 15) & ~15);
+          for (int t = 0; t < 8 && ns.e0 + t < ns.ne; ++t)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(
+                             ns.in + (ns.e0 + t) * ns.stride),
+                         "r"(bytes)
+                         : "memory");
+        }
         for (int j = 0; j < 4; ++j) {
           tc::mbar_wait(staged, j & 1);
           tma_store_4d(second ? &om2 : &om1, sStage, e0, 0, 0, 4 * j);
@@ -456,6 +394,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc::bulk_wait0();
     }
+  } else if (warp > kWorkers + 1) {
+    // ------------------------------ input warps -------------------------------
+    // slice j of tile `it` once the last pass of tile it - 1 has read it; the
+    // loads of the next slice are in flight while waiting
+    const int i0 = (warp - kWorkers - 2) * 32 + lane;
+    const uint32_t p3a = tc::smem_u32(p3done);
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
+      const TileSrc s = tile_src(a, tile);
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+#pragma unroll 1
+        for (int part = 0; part < a.kc1 / 2; ++part) {
+          LoadBuf lb;
+          slice_load(a, s, j, i0 + part * kLT * kLoadItems, lb);
+          if (part == 0 && it > 0) tc::mbar_wait_sleep_a(p3a + 8 * j, (it - 1) & 1);
+          slice_store(sdata, j, i0 + part * kLT * kLoadItems, lb);
+        }
+        tc::fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&ready[j]);
+      }
+    }
   } else {
     // --------------------------------- workers --------------------------------
     const int wk = warp - 1;          // 0 .. kWorkers - 1
@@ -463,7 +424,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int h = wk >> 2;            // column part: kVpm of the 16 outputs of each MMA
     const int R = 32 * q + lane;      // operand row = TMEM lane
     const int u = R >> 3, t = R & 7;  // row digit, transform of the tile
-    const int w = wk * 32 + lane;     // worker thread index
     const int c0 = kVpm * h;          // first output column of this thread
     const int ur = (int)(__brev((unsigned)u) >> 28);  // brev4(u)
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(4 * c0);
@@ -473,51 +433,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sRow = sdata + (uint32_t)(c0 * 8 + t) * 16u;
     const uint32_t sRowR = sdata + (uint32_t)t * 16u;
     const uint32_t sSt = sStage + (uint32_t)(c0 * 128 + u * 8 + t) * 4u;  // [s][c][u][t]
-    FwdPre fpre;
-    InvPre ipre;
-    uint32_t yp[4][kVpm];  // inverse: the even chunk's outputs, written with the odd one
-    int it = 0;
-    long long tile = blockIdx.x;
-    if (tile < a.tiles) {
-      const TileSrc s0 = tile_src(a, tile);
-      for (int j = 0; j < 4; ++j) {
-        if (DIR == 0) {
-          fwd_load(a, s0, j, w, fpre);
-          fwd_store(a, sdata, j, w, fpre);
-        } else {
-          inv_load(s0, j, w, ipre);
-          inv_store(sdata, j, w, ipre);
-        }
-        tc::fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&ready[j]);
-      }
-    }
-    for (; tile < a.tiles; tile += gridDim.x, ++it) {
-      const TileSrc src = tile_src(a, tile);
-      const long long nxt = tile + gridDim.x;
-      const bool has_next = nxt < a.tiles;
-      const TileSrc nsrc = tile_src(a, has_next ? nxt : tile);
+    for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x) {
 #pragma unroll
       for (int pass = 0; pass < 3; ++pass) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const int buf = j & 1;
-          if (pass == 2 && has_next) {
-            if (DIR == 0)
-              fwd_load(a, nsrc, j, w, fpre);
-            else
-              inv_load(nsrc, j, w, ipre);
-          }
           tc::mbar_wait(&full[buf], (j >> 1) & 1);
           tc::fence_after_sync();
           uint32_t y[4][kVpm];
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
-            // two MMAs at a time (register budget: 18 warps -> 96 per thread)
+            // two MMAs at a time (register budget: 20 warps -> 96 per thread)
             uint32_t v[2][4 * kVpm];
-            tmem_ldv(tl + buf * 256 + (2 * hf) * 64, v[0]);
-            tmem_ldv(tl + buf * 256 + (2 * hf + 1) * 64, v[1]);
+            tmem_ld16_nw(tl + buf * 256 + (2 * hf) * 64, v[0]);
+            tmem_ld16_nw(tl + buf * 256 + (2 * hf + 1) * 64, v[1]);
             tc::tmem_wait_ld();
             if (hf == 1) {
               tc::fence_before_sync();
@@ -532,17 +462,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                           v[ss][4 * i + 3], p, negp, w16s);
           }
           if (pass < 2) {
-            // forward: w^((u + 16 m) col) in P1 (row digit a = u, MMA digit b),
-            // w^(16 m col) in P2 (MMA digit a); inverse: row 16 k1 (k1 =
-            // brev4(m)), column a in I1; row 16 k0 + u (k0 = brev4(m)),
-            // column b in I2
-            const bool own_row = DIR == 0 ? pass == 0 : pass == 1;
+            // w^((u + 16 m) col) in P1 (row digit a = u, MMA digit b),
+            // w^(16 m col) in P2 (MMA digit a)
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-              const int md = DIR == 0 ? 4 * j + s : brev4c(4 * j + s);
-              const int m = 16 * md + (own_row ? u : 0);  // m & 7 == (own_row ? u & 7 : 0)
+              const int m = 16 * (4 * j + s) + (pass == 0 ? u : 0);  // m & 7 == (pass ? 0 : u & 7)
               const uint32_t rb = sTw + (uint32_t)m * 128u;
-              const int sw = own_row ? (u & 7) : 0;
+              const int sw = pass == 0 ? (u & 7) : 0;
 #pragma unroll
               for (int i = 0; i < kVpm; i += 2) {
                 const uint4 c = lds128(rb + ((uint32_t)(((c0 + i) >> 1) ^ sw) << 4));
@@ -556,12 +482,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < kVpm; ++i)
                 sts128(sRow + mb + (uint32_t)i * 128u, y[0][i], y[1][i], y[2][i], y[3][i]);
-            } else if (DIR == 1) {
-              // I3 operand: matrix u (= a), row (b = c0 + i, t), K chunk j
-              const uint32_t mb = off_s(u, j, 0);
-#pragma unroll
-              for (int i = 0; i < kVpm; ++i)
-                sts128(sRow + mb + (uint32_t)i * 128u, y[0][i], y[1][i], y[2][i], y[3][i]);
             } else {
               // P3 operand: matrix brev4(u) (u = k0), row (brev4(k1), t), K chunk j
               const uint32_t mb = off_s(ur, j, 0);
@@ -571,84 +491,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                 sts128(sRowR + mb + rg * 128u, y[0][i], y[1][i], y[2][i], y[3][i]);
               }
             }
+          } else if (a.tma_out) {
+            // position c + 16 u + 256 (4 j + s) (= brev12 of the point index);
+            // staging [s][c][u][t]: one TMA box (8 entries x 1024 positions)
+            tc::mbar_wait(stfree, (j & 1) ^ 1);
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+#pragma unroll
+              for (int i = 0; i < kVpm; ++i)
+                sts32(sSt + (uint32_t)(s * 2048 + i * 128) * 4u, y[s][i]);
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(staged);
           } else {
-            // forward evaluations stay unreduced (< 2^31 + p): their only
-            // consumers are the int8 tensor-core products, whose limb
-            // identity takes any 32-bit residue (tc_pair.cu, tc_grouped.cu);
-            // the inverse's coefficients are reduced below p
-            if (DIR == 1) {
-#pragma unroll
-              for (int s = 0; s < 4; ++s)
-#pragma unroll
-                for (int i = 0; i < kVpm; ++i) {
-                  uint32_t x = y[s][i];
-                  x = min(x, x - p);
-                  y[s][i] = min(x, x - p);
-                }
-            }
-            const long long e = src.e0 + t;
-            if (DIR == 1) {
-              // coefficient a + 16 b + 256 c: a = MMA digit, b = u, c = column.
-              // Chunks are written in pairs: 8 consecutive coefficients per
-              // column from one thread at once
-              if ((j & 1) == 0) {
-#pragma unroll
-                for (int s = 0; s < 4; ++s)
-#pragma unroll
-                  for (int i = 0; i < kVpm; ++i) yp[s][i] = y[s][i];
-              } else if (e < src.ne) {
-                uint32_t* dst = src.out + e * a.out_stride;
-#pragma unroll
-                for (int i = 0; i < kVpm; ++i) {
-                  const int n = 8 * (j >> 1) + 16 * u + 256 * (c0 + i);
-                  if (a.vec && n + 7 < a.len) {
-                    asm volatile(
-                        "st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + n),
-                        "r"(yp[0][i]), "r"(yp[1][i]), "r"(yp[2][i]), "r"(yp[3][i]), "r"(y[0][i]),
-                        "r"(y[1][i]), "r"(y[2][i]), "r"(y[3][i])
-                        : "memory");
-                  } else {
-#pragma unroll
-                    for (int s = 0; s < 4; ++s)
-                      if (n + s < a.len) dst[n + s] = yp[s][i];
-#pragma unroll
-                    for (int s = 0; s < 4; ++s)
-                      if (n + 4 + s < a.len) dst[n + 4 + s] = y[s][i];
-                  }
-                }
-              }
-            } else if (tma_out) {
-              // position c + 16 u + 256 (4 j + s) (= brev12 of the point index);
-              // staging [s][c][u][t]: one TMA box (8 entries x 1024 positions)
-              tc::mbar_wait(stfree, (j & 1) ^ 1);
-#pragma unroll
-              for (int s = 0; s < 4; ++s)
-#pragma unroll
-                for (int i = 0; i < kVpm; ++i)
-                  sts32(sSt + (uint32_t)(s * 2048 + i * 128) * 4u, y[s][i]);
-              tc::fence_proxy_async();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(staged);
-            } else if (e < src.ne) {
-              // each warp store writes 4 full 32-byte sectors
-              const long long ne = src.ne;
-              uint32_t* pj = src.out + e + (16 * u + c0 + 1024 * j) * ne;
+            // each warp store writes 4 full 32-byte sectors
+            const bool second = tile >= a.tiles1;
+            const long long ne = second ? a.n2 : a.n1;
+            const long long e = (second ? tile - a.tiles1 : tile) * 8 + t;
+            if (e < ne) {
+              uint32_t* pj = (second ? a.out2 : a.out1) + e + (16 * u + c0 + 1024 * j) * ne;
 #pragma unroll
               for (int s = 0; s < 4; ++s) {
                 uint32_t* ps = pj + 256 * s * ne;
 #pragma unroll
                 for (int i = 0; i < kVpm; ++i) ps[i * ne] = y[s][i];
               }
-            }
-            if (has_next) {
-              // the last pass's MMAs of chunk j have read slice j: refill it
-              if (DIR == 0)
-                fwd_store(a, sdata, j, w, fpre);
-              else
-                inv_store(sdata, j, w, ipre);
-              tc::fence_proxy_async();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&ready[j]);
             }
           }
         }
@@ -694,61 +561,14 @@ bool out_map(CUtensorMap* m, uint32_t* base, long long ne) {
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int DIR>
-int launch_mma(MmaArgs a, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma_kernel<DIR>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    attr = true;
-  }
-  CUtensorMap om1{}, om2{};
-  a.tma_out = 0;
-  if (DIR == 0 && option(kOptNttPmLsu) == 0 && out_map(&om1, a.out1, a.n1) &&
-      (a.n2 == 0 || out_map(&om2, a.out2, a.n2)))
-    a.tma_out = 1;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long grid = a.tiles < sms ? a.tiles : sms;
-  FPM_CUDA_TRY(launch_pdl(ntt_mma_kernel<DIR>, dim3((unsigned)grid), dim3(kThreads), kSmem, st,
-                          a, om1, om2));
-  FPM_LAUNCH_CHECK();
-  return kOk;
-}
-
 bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15) == 0; }
 
 }  // namespace
 
-static bool mma_prime_ok(const PrimeSet& ps) {
-  if (option(kOptNttNoMma) != 0) return false;
-  if (ps.count != 1 || ps.pr[0].mma == nullptr) return false;
-  return ps.pr[0].p > (1u << 30) && ps.pr[0].p < (1u << 31);
-}
-
-bool ntt_mma_inv_ok(int logn, const NttInvArgs& a, const PrimeSet& ps) {
-  if (logn != 12 || !mma_prime_ok(ps)) return false;
-  return a.pm && !a.natural && a.off == 0 && a.scale == 1 && a.out_len > 0 && a.out_len <= 4096 &&
-         a.n_entries > 0 && a.n_entries <= (1 << 20);
-}
-
-int launch_ntt_inv_mma(const NttInvArgs& f, const PrimeSet& ps, cudaStream_t st) {
-  MmaArgs a{};
-  a.in1 = f.in; a.out1 = f.out; a.n1 = f.n_entries; a.n2 = 0;
-  a.out_stride = f.out_stride;
-  a.len = f.out_len;
-  a.kc1 = 4;
-  a.vec = (f.out_stride % 8 == 0) && (((uintptr_t)f.out & 31) == 0);
-  a.tiles1 = a.tiles = (a.n1 + 7) / 8;
-  a.p = ps.pr[0].p;
-  a.w16s = (uint32_t)((((uint64_t)1) << 48) / a.p);
-  a.tab = ps.pr[0].mma;
-  return launch_mma<1>(a, st);
-}
-
 bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps) {
-  if (logn != 12 || !mma_prime_ok(ps)) return false;
+  if (logn != 12 || option(kOptNttNoMma) != 0) return false;
+  if (ps.count != 1 || ps.pr[0].mma == nullptr) return false;
+  if (ps.pr[0].p <= (1u << 30) || ps.pr[0].p >= (1u << 31)) return false;
   // 32-bit point offsets: 4096 * entries < 2^32
   return a.pm && !a.natural && !a.fold && !a.in64 && !a.reduce && a.len > 0 && a.len <= 4096 &&
          a.n_entries <= (1 << 20) && a.n_entries2 <= (1 << 20);
@@ -769,7 +589,24 @@ int launch_ntt_fwd_mma(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t st)
   a.p = ps.pr[0].p;
   a.w16s = (uint32_t)((((uint64_t)1) << 48) / a.p);
   a.tab = ps.pr[0].mma;
-  return launch_mma<0>(a, st);
+  static bool attr = false;
+  if (!attr) {
+    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmem));
+    attr = true;
+  }
+  CUtensorMap om1{}, om2{};
+  if (option(kOptNttPmLsu) == 0 && out_map(&om1, a.out1, a.n1) &&
+      (a.n2 == 0 || out_map(&om2, a.out2, a.n2)))
+    a.tma_out = 1;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long grid = a.tiles < sms ? a.tiles : sms;
+  FPM_CUDA_TRY(launch_pdl(ntt_mma_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, a, om1,
+                          om2));
+  FPM_LAUNCH_CHECK();
+  return kOk;
 }
 
 }  // namespace fpm

@@ -55,23 +55,6 @@ def test_mma_ntt_extreme_operands():
     assert np.all(got == got[0, 0][None, None, :])
 
 
-@pytest.mark.parametrize("la,lb", [(2048, 2048), (2049, 2048), (1000, 777)])
-def test_mma_inverse_opt_in(la, lb):
-    """the tensor-core inverse (option ntt_mma_inv, off by default: measured
-    slower than the Shoup inverse) reproduces the default path bit-exactly on
-    4095-word (unaligned) and 4096-word (32-byte aligned) output rows"""
-    p = P31
-    A = _rand(p, (40, 36, la), 11)
-    B = _rand(p, (36, 48, lb), 12)
-    ref = _mul(p, A, B)
-    _lib.set_option("ntt_mma_inv", 1)
-    try:
-        got = _mul(p, A, B)
-    finally:
-        _lib.set_option("ntt_mma_inv", 0)
-    assert np.array_equal(got, ref)
-
-
 def test_mma_ntt_matches_dif_kernels():
     p = P31
     A = _rand(p, (64, 48, 2048), 7)
