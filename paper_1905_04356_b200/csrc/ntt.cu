@@ -384,7 +384,9 @@ int inv_impl(const NttInvArgs& a, const PrimeSet& ps, cudaStream_t st) {
 
 int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStream_t st) {
   // tensor-core transforms (same DIF point order as the kernels below)
-  if (ntt_mma_fwd_ok(logn, a_in, ps)) return launch_ntt_fwd_mma(a_in, ps, st);
+  if (ntt_mma_fwd_ok(logn, a_in, ps))
+    return option(kOptNttMmaR16) != 0 ? launch_ntt_fwd_mma(a_in, ps, st)
+                                      : launch_ntt_fwd_mma64(a_in, ps, st);
   const bool no_persist = option(kOptNttGeneric) != 0;
   if (!no_persist && ntt_tma_fwd_ok(logn, a_in)) return launch_ntt_fwd_tma(logn, a_in, ps, st);
   if (a_in.n_entries2 > 0) {

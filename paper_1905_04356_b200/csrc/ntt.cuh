@@ -86,6 +86,8 @@ int launch_ntt_inv_tma(int logn, const NttInvArgs& a, const PrimeSet& ps, cudaSt
 // the kernels above (launch_ntt_fwd picks it when it applies)
 bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps);
 int launch_ntt_fwd_mma(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
+// the same transforms in two radix-64 passes (ntt_mma64.cu); the default
+int launch_ntt_fwd_mma64(const NttFwdArgs& a, const PrimeSet& ps, cudaStream_t st);
 
 // word offset of the 16-byte piece holding points x0 .. x0+3 (x0 % 4 == 0)
 // of entry e in the blocked eval layout E[N / 2^pl][n_entries][2^pl]

@@ -307,6 +307,7 @@ int Context::plan(uint32_t p, int logn, const Plan** out) {
   if (logn == 12 && p > (1u << 30) && p < (1u << 31)) {
     std::vector<uint8_t> tab;
     mma_ntt_tables(p, (uint32_t)omega, &tab);
+    mma64_ntt_tables(p, (uint32_t)omega, &tab);  // appended at kMma64TabOff
     FPM_CUDA_TRY(cudaMalloc(&pl.mma, tab.size()));
     FPM_CUDA_TRY(cudaMemcpy(pl.mma, tab.data(), tab.size(), cudaMemcpyHostToDevice));
   }
@@ -393,6 +394,7 @@ const OptDef kOptDefs[kOptCount] = {
     {"no_pdl", 0},      {"host_blocks", 0},   {"no_chirp", 0},     {"ntt_generic", 0},
     {"ntt_no_tma", 0},  {"ntt_no_small", 0},  {"ntt_pm_lsu", 0},   {"ntt_pm_scatter", 0},
     {"pmbasis_leaf", 8}, {"pmbasis_host_sync", 0}, {"ntt_no_mma", 0}, {"tc_no_pair", 0}, {"tc_pair1", 0},
+    {"ntt_mma_r16", 0},
 };
 std::atomic<long long> g_opt[kOptCount] = {};
 std::atomic<bool> g_opt_init{false};

@@ -30,8 +30,13 @@ struct BigPlan {
   uint32_t ninv = 0, ninv_sh = 0;
 };
 
-// host tables of the tensor-core NTT for (p, N = 4096) (ntt_mma.cu)
+// host tables of the tensor-core NTT for (p, N = 4096): the radix-16 kernel's
+// (ntt_mma.cu, 40 KB) followed by the radix-64 kernel's (ntt_mma64.cu: 64 KB B
+// operand + 16 KB twiddles, appended at kMma64TabOff)
+constexpr uint32_t kMma64TabOff = 8192 + 32768;
+constexpr uint32_t kMma64TabBytes = 65536 + 16384;
 void mma_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out);
+void mma64_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out);
 
 class Context {
  public:
