@@ -156,6 +156,7 @@ enum Option : int {
   kOptTcNoPair,           // "tc_no_pair": tc_grouped instead of tc_pair for 128 < m <= 256
   kOptTcPair1,            // "tc_pair1": one-SM tc_pair instead of the CTA-pair kernel
   kOptNttMmaR16,          // "ntt_mma_r16": three radix-16 passes (ntt_mma.cu), not two radix-64
+  kOptNttMmaDbg,          // "ntt_mma_dbg": timing experiments of ntt_mma64.cu (WRONG results)
   kOptCount
 };
 long long option(Option o);

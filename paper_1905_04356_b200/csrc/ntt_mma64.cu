@@ -122,6 +122,7 @@ struct Mma64Args {
   uint32_t negp, zero;               // 2^32 - p; 0 (opaque: keeps 3-input adds on the ALU pipe)
   const uint8_t* tab;
   int tma_out;                       // point-major output by TMA stores
+  int dbg;                           // timing experiments (option ntt_mma_dbg): 1 = no input loads
 };
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, uint32_t z,
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   // full[2], empty[2], slice ready[4], P1 done, P2 MMAs done, staged[2], stage free[2];
   // TMEM base
-  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 8;
+  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 16;  // pdone[4]
   uint64_t *p2done = bars + 9, *staged = bars + 10, *stfree = bars + 12;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -285,8 +286,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&staged[b], kWorkers);
       tc::mbar_init(&stfree[b], 1);
     }
-    for (int j = 0; j < 4; ++j) tc::mbar_init(&ready[j], kLoaders);
-    tc::mbar_init(pdone, kWorkers);
+    for (int j = 0; j < 4; ++j) {
+      tc::mbar_init(&ready[j], kLoaders);
+      tc::mbar_init(&pdone[j], kWorkers);
+    }
     tc::mbar_init(p2done, 1);
     tc::fence_mbar_init();
   }
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int s = 0; s < 4; ++s) {
           const int buf = s & 1;
           tc::mbar_wait_spin(tc::smem_u32(&empty[buf]), ((s >> 1) & 1) ^ 1);
-          tc::mbar_wait_spin(tc::smem_u32(&ready[s]), it & 1);
+          if (!(a.dbg & 2)) tc::mbar_wait_spin(tc::smem_u32(&ready[s]), it & 1);
           tc::fence_after_sync();
           const uint32_t d = tmem + buf * 256;
           for (int i = 0; i < ks1; ++i)
@@ -322,9 +325,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                        dB + ((uint32_t)(i * 256) >> 4), idesc, i > 0 ? 1u : 0u);
           tc::commit(&full[buf]);
         }
-        // P2: chunk s reads its 8 KB of every slice
-        tc::mbar_wait_spin(tc::smem_u32(pdone), it & 1);
-        tc::fence_after_sync();
+        // P2: chunk s reads its 8 KB of every slice; the K steps of slice sl
+        // (chunk 0) start as soon as the P1 epilogue of chunk sl has written it
 #pragma unroll 1
         for (int s = 0; s < 4; ++s) {
           const int buf = s & 1;
@@ -332,9 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::fence_after_sync();
           const uint32_t d = tmem + buf * 256;
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
+          for (int i = 0; i < 8; ++i) {
+            if (s == 0 && (i & 1) == 0) {
+              tc::mbar_wait_spin(tc::smem_u32(&pdone[i >> 1]), it & 1);
+              tc::fence_after_sync();
+            }
             tc::mma_u8(d, dA + ((uint32_t)((i >> 1) * 32768 + s * 8192 + (i & 1) * 4096) >> 4),
                        dB + ((uint32_t)(i * 256) >> 4), idesc, i > 0 ? 1u : 0u);
+          }
           tc::commit(&full[buf]);
         }
         tc::commit(p2done);  // the data region may be refilled
@@ -379,9 +386,48 @@ __global__ void __launch_bounds__(kThreads, 1)
     // loads of the first round are in flight while waiting
     const int i0 = (warp - kWorkers - 2) * 32 + lane;
     const uint32_t p2a = tc::smem_u32(p2done);
+    // a thread's items of a round: (t, aq) fixed, kc = kcb + 2 r (+ 8 part)
+    const int lt = i0 & 7, aq = (i0 >> 3) & 3, kcb = i0 >> 5;
+    const uint32_t dst0 = sdata + (uint32_t)(kcb * 2048 + (4 * aq) * 128 + lt * 16);
+    // rows of whole 64-word blocks, 16-byte aligned: every load is one
+    // predicated LDG.128 at a constant offset from the tile's row pointer
+    const bool fast = a.vec && (a.len & 63) == 0;
     int it = 0;
     for (long long tile = blockIdx.x; tile < a.tiles; tile += gridDim.x, ++it) {
       const TileSrc s = tile_src(a, tile);
+      if (fast) {
+        const bool valid = s.e0 + lt < s.ne && !(a.dbg & 1);
+        const uint4* src =
+            reinterpret_cast<const uint4*>(s.in + (s.e0 + lt) * s.stride + 4 * aq) + 64 * kcb;
+#pragma unroll
+        for (int sl = 0; sl < 4; ++sl) {
+#pragma unroll 1
+          for (int part = 0; part < a.kc1 / 8; ++part) {
+            const int lim = (a.len >> 6) - 4 * kcb - 32 * part;  // valid b: 8 r + i < lim
+            const uint4* sp = src + 512 * part + 4 * sl;
+            uint4 g[4][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                g[r][i] = (valid && 8 * r + i < lim) ? __ldg(sp + 128 * r + 16 * i)
+                                                     : make_uint4(0u, 0u, 0u, 0u);
+            if (sl == 0 && part == 0 && it > 0) tc::mbar_wait_sleep_a(p2a, (it - 1) & 1);
+            const uint32_t d = dst0 + (uint32_t)(sl * 32768 + part * 16384);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+              sts128(d + r * 4096, g[r][0].x, g[r][1].x, g[r][2].x, g[r][3].x);
+              sts128(d + r * 4096 + 128, g[r][0].y, g[r][1].y, g[r][2].y, g[r][3].y);
+              sts128(d + r * 4096 + 256, g[r][0].z, g[r][1].z, g[r][2].z, g[r][3].z);
+              sts128(d + r * 4096 + 384, g[r][0].w, g[r][1].w, g[r][2].w, g[r][3].w);
+            }
+          }
+          tc::fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&ready[sl]);
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int sl = 0; sl < 4; ++sl) {
 #pragma unroll 1
@@ -476,12 +522,14 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          if (pass == 0) {
+            // slice s now holds its part of the P2 operands
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&pdone[s]);
+          }
         }
-        if (pass == 0) {
-          tc::fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(pdone);
-        }
+
       }
     }
     pdl_trigger();
@@ -542,6 +590,7 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   a.pinv = inv;
   a.negp = 0u - a.p;
   a.zero = 0;
+  a.dbg = (int)option(kOptNttMmaDbg);
   a.tab = ps.pr[0].mma + kMma64TabOff;
   static bool attr = false;
   if (!attr) {
