@@ -173,6 +173,7 @@ __device__ __forceinline__ uint32_t prmt0(uint32_t a, uint32_t sel) {
 // (L - p if L >= p), so L + r < 2^32 - 2^24 - p + p.
 // z = 0 at run time: a 3-input add is an ALU IADD3, where ptxas would issue a
 // 2-input one as IMAD.IADD on the multiply pipe that the epilogue saturates.
+template <bool RL>
 __device__ __forceinline__ uint32_t fold4w(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
                                            uint32_t p, uint32_t negp, uint32_t w16s, uint32_t z) {
   const uint32_t H = d2 + prmt0(d3, 0x2104) + z;        // d2 + (d3 << 8)
@@ -180,7 +181,7 @@ __device__ __forceinline__ uint32_t fold4w(uint32_t d0, uint32_t d1, uint32_t d2
   uint32_t r = prmt0(H, 0x1044) + q * negp;             // (H << 16) - q p, in [0, 2p)
   r = min(r, r - p);
   uint32_t L = d0 + prmt0(d1, 0x2104) + z;              // d0 + (d1 << 8)
-  L = min(L, L - p);
+  if (RL) L = min(L, L - p);  // !RL: the planes are < 2^23 (K' = 128), L < 2^31 + 2^23
   return L + r + z;
 }
 // Montgomery product y W 2^-32 mod p (y < 2^32, W < p) in (0, 2p)
@@ -259,6 +260,7 @@ __host__ __device__ constexpr int brev3c(int x) {
   return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1);
 }
 
+template <bool kHalfK>  // P1 reads only the inputs b < 32 (len <= 2048): K' = 128
 __global__ void __launch_bounds__(kThreads, 1)
     ntt_mma64_kernel(const __grid_constant__ Mma64Args a, const __grid_constant__ CUtensorMap om1,
                      const __grid_constant__ CUtensorMap om2) {
@@ -475,23 +477,41 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int buf = s & 1;
           tc::mbar_wait(&full[buf], (s >> 1) & 1);
           tc::fence_after_sync();
+          // the chunk's 64 columns in quarters of 4 values through two register
+          // buffers: the next quarter's TMEM load is in flight while one is folded
+          const uint32_t tb = tl + buf * 256;
+          uint32_t va[16], vb[16], y[8];
+          tmem_ld16_nw(tb, va);
+          tmem_ld16_nw(tb + 16, vb);
+          tc::tmem_wait_ld();
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
-            uint32_t v[2][16];
-            tmem_ld16_nw(tl + buf * 256 + 32 * g, v[0]);
-            tmem_ld16_nw(tl + buf * 256 + 32 * g + 16, v[1]);
-            tc::tmem_wait_ld();
-            if (g == 1) {
-              tc::fence_before_sync();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&empty[buf]);
-            }
-            uint32_t y[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
-              y[i] = fold4w(v[i >> 2][4 * (i & 3)], v[i >> 2][4 * (i & 3) + 1],
-                            v[i >> 2][4 * (i & 3) + 2], v[i >> 2][4 * (i & 3) + 3], p, negp, w16s,
-                            z);
+            for (int hq = 0; hq < 2; ++hq) {
+              const uint32_t(&v)[16] = hq == 0 ? va : vb;
+              // P1 with K' = 128: D_r < 2^23, so d0 + 2^8 d1 + r < 2^31 + 2^23 + p
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                y[4 * hq + i] = (pass == 0 && kHalfK)
+                                    ? fold4w<false>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                                                    v[4 * i + 3], p, negp, w16s, z)
+                                    : fold4w<true>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                                                   v[4 * i + 3], p, negp, w16s, z);
+              if (g == 0) {
+                // refill this buffer with the matching quarter of the second half
+                if (hq == 0) {
+                  tmem_ld16_nw(tb + 32, va);
+                } else {
+                  tc::tmem_wait_ld();  // va (third quarter) has landed
+                  tmem_ld16_nw(tb + 48, vb);
+                }
+              } else if (hq == 0) {
+                tc::tmem_wait_ld();    // vb: the accumulator is read out
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&empty[buf]);
+              }
+            }
             if (pass == 0) {
               const uint32_t nb = sNext + (uint32_t)(s * 32768 + g * 8192);
 #pragma unroll
@@ -529,7 +549,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) tc::mbar_arrive(&pdone[s]);
           }
         }
-
       }
     }
     pdl_trigger();
@@ -594,8 +613,10 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   a.tab = ps.pr[0].mma + kMma64TabOff;
   static bool attr = false;
   if (!attr) {
-    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kSmem));
+    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr = true;
   }
   CUtensorMap om1{}, om2{};
@@ -606,8 +627,12 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = a.tiles < sms ? a.tiles : sms;
-  FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, a,
-                          om1, om2));
+  if (a.kc1 == 8)
+    FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel<true>, dim3((unsigned)grid), dim3(kThreads), kSmem, st,
+                            a, om1, om2));
+  else
+    FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel<false>, dim3((unsigned)grid), dim3(kThreads), kSmem,
+                            st, a, om1, om2));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
