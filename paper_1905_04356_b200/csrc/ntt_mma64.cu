@@ -270,7 +270,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   // full[2], empty[2], slice ready[4], P1 done, P2 MMAs done, staged[2], stage free[2];
   // TMEM base
-  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 16;  // pdone[4]
+  uint64_t *full = bars, *empty = bars + 2, *ready = bars + 4, *pdone = bars + 16;  // pdone[3]
+  uint64_t* pd3 = bars + 20;  // pd3[4]: slice 3's part of P2 operand s' (8 warps, one half each)
   uint64_t *p2done = bars + 9, *staged = bars + 10, *stfree = bars + 12;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < 4; ++j) {
       tc::mbar_init(&ready[j], kLoaders);
       tc::mbar_init(&pdone[j], kWorkers);
+      tc::mbar_init(&pd3[j], kWorkers / 2);
     }
     tc::mbar_init(p2done, 1);
     tc::fence_mbar_init();
@@ -328,7 +330,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::commit(&full[buf]);
         }
         // P2: chunk s reads its 8 KB of every slice; the K steps of slice sl
-        // (chunk 0) start as soon as the P1 epilogue of chunk sl has written it
+        // (chunk 0) start as soon as the P1 epilogue of chunk sl has written it,
+        // those of slice 3 as soon as the 8 warps that write operand s have
 #pragma unroll 1
         for (int s = 0; s < 4; ++s) {
           const int buf = s & 1;
@@ -337,8 +340,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t d = tmem + buf * 256;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (s == 0 && (i & 1) == 0) {
+            if (s == 0 && i < 6 && (i & 1) == 0) {
               tc::mbar_wait_spin(tc::smem_u32(&pdone[i >> 1]), it & 1);
+              tc::fence_after_sync();
+            }
+            if (i == 6) {
+              // operand s of slice 3: the half s & 1 of the warps h >> 1 = s >> 1
+              tc::mbar_wait_spin(tc::smem_u32(&pd3[s]), it & 1);
               tc::fence_after_sync();
             }
             tc::mma_u8(d, dA + ((uint32_t)((i >> 1) * 32768 + s * 8192 + (i & 1) * 4096) >> 4),
@@ -519,6 +527,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t W = __shfl_sync(0xffffffffu, twr[2 * s + g], (lane & 24) | i);
                 sts32(nb + (uint32_t)(2 * brev3c(i)) * 128u, mont(y[i], W, p, pinv));
               }
+              if (s == 3) {
+                // this half completes the P2 operand g + 2 (h >> 1)
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&pd3[g + 2 * (h >> 1)]);
+              }
             } else if (a.tma_out) {
               // buffer g, its s-th use of the tile (4 per tile)
               tc::mbar_wait(&stfree[g], (s & 1) ^ 1);
@@ -542,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
-          if (pass == 0) {
+          if (pass == 0 && s < 3) {
             // slice s now holds its part of the P2 operands
             tc::fence_proxy_async();
             __syncwarp();
