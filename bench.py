@@ -287,11 +287,11 @@ def roofline_report(cfg, cfgname, avg, sbytes):
             "algorithmic_bytes": b, "ms": round(ms, 5), "peak_source": hsrc}
     if dom == "ntt":
         roof["note"] = ("HBM fraction per SURVEY 8(d).  The NTT kernels are bound by their "
-                        "CUDA-core instruction stream, not HBM: the 4096-point forward runs its "
-                        "radix-16 DFTs on the int8 tensor cores (ntt_mma.cu) and is limited by "
-                        "the limb fold + twiddle epilogue (IMAD.HI at quarter rate); the inverse "
-                        "(Shoup butterflies) by the heavy FMA pipe; `compute` gives ncu "
-                        "pipe/issue utilisation, DESIGN.md 4")
+                        "CUDA-core instruction stream, not HBM: the 4096-point forward runs as "
+                        "two radix-64 passes on the int8 tensor cores (ntt_mma64.cu) and is "
+                        "limited by the limb fold + twiddle epilogue and the TMA store of the "
+                        "32-byte point rows; the inverse (Shoup butterflies) by the heavy FMA "
+                        "pipe; `compute` gives ncu pipe/issue utilisation, DESIGN.md 4")
         pipes = read_pipes().get(cfgname, {})
         comp = {}
         for st in ("ntt_fwd", "ntt_inv"):

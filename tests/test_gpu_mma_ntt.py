@@ -1,4 +1,4 @@
-"""Tensor-core NTT path (csrc/ntt_mma.cu): products whose transforms have
+"""Tensor-core NTT path (csrc/ntt_mma64.cu, and ntt_mma.cu behind option ntt_mma_r16): products whose transforms have
 N = 4096 points in the point-major layout (m > 32, 2^30 < p < 2^31) run all
 three transforms on tcgen05.  Bit-exact against the oracle (restatement of
 polmat._pm_mul_ntt, /root/reference/pkg/src/fpmat/polmat.py:290-308) and
@@ -66,3 +66,37 @@ def test_mma_ntt_matches_dif_kernels():
     finally:
         _lib.set_option("ntt_no_mma", 0)
     assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("la,lb", [(2048, 2048), (3000, 1097)])
+def test_mma_ntt_radix16_option_matches(la, lb):
+    """the three-pass radix-16 kernel (option ntt_mma_r16) and the default
+    two-pass radix-64 kernel produce the same product"""
+    p = P31
+    A = _rand(p, (40, 24, la), 11)
+    B = _rand(p, (24, 48, lb), 12)
+    got = _mul(p, A, B)
+    _lib.set_option("ntt_mma_r16", 1)
+    try:
+        ref = _mul(p, A, B)
+    finally:
+        _lib.set_option("ntt_mma_r16", 0)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got[:1, :1], O.pm_mul(p, A[:1], B[:, :1]))
+
+
+def test_mma_ntt_extreme_operands_long():
+    """all coefficients p - 1 with more than 2048 coefficients: the first pass
+    runs with K' = 256 (largest byte-plane sums D_r = 256 * 255 * byte)"""
+    p = P31
+    A = _rand(p, (40, 16, 3000), 0, extreme=True)
+    B = _rand(p, (16, 40, 1097), 0, extreme=True)
+    got = _mul(p, A, B)
+    assert np.array_equal(got[:1, :1], O.pm_mul(p, A[:1], B[:, :1]))
+    assert np.all(got == got[0, 0][None, None, :])
+    # 0x77FFFFFF < p: three 0xFF bytes in every input word
+    A[:] = 0x77FFFFFF
+    B[:] = 0x77FFFFFF
+    got = _mul(p, A, B)
+    assert np.array_equal(got[:1, :1], O.pm_mul(p, A[:1], B[:, :1]))
+    assert np.all(got == got[0, 0][None, None, :])

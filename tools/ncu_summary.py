@@ -44,7 +44,7 @@ METRICS = [
     "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
 ]
 
-STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_mma_kernel<0>": "ntt_fwd", "ntt_mma_kernel<1>": "ntt_inv",
+STAGE_OF = {"ntt_fwd": "ntt_fwd", "ntt_mma_kernel<0>": "ntt_fwd", "ntt_mma64_kernel": "ntt_fwd", "ntt_mma_kernel<1>": "ntt_inv",
             "ntt_inv": "ntt_inv", "pointwise_cc": "pointwise", "tc_pair": "pointwise_tc",
             "tc_pointwise": "pointwise_tc", "tc_grouped": "pointwise_tc", "tc_pq": "pointwise_tc",
             "crt_kernel": "crt"}

@@ -44,7 +44,7 @@ def run(name):
 
 def stage_of(kernel, fwd_seen):
     k = kernel
-    if "ntt_fwd" in k or "ntt_mma_kernel<0>" in k or "ntt_mma_fwd" in k:
+    if "ntt_fwd" in k or "ntt_mma_kernel<0>" in k or "ntt_mma_fwd" in k or "ntt_mma64" in k:
         return "ntt_fwd"
     if "ntt_mma_kernel<1>" in k:
         return "ntt_inv"

@@ -20,6 +20,6 @@ for C in cfg5 cfg2 cfg3 cfg1; do
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
       --csv --log-file $O/traffic_$C.csv python tools/ncu_traffic.py run $C > $O/traffic_$C.log 2>&1
 done
-ncu --set full --import-source on --clock-control none -k regex:"ntt_mma_kernel|tc_pair2_kernel|ntt_inv_persist" \
+ncu --set full --import-source on --clock-control none -k regex:"ntt_mma64_kernel|tc_pair2_kernel|ntt_inv_persist" \
     -c 3 -o $O/cfg5_full python tools/run_one.py cfg5 1 > $O/cfg5_full.log 2>&1
 echo done > $O/DONE
