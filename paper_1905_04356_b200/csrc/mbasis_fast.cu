@@ -39,6 +39,18 @@ struct F31 {
   uint32_t r2;       // 2^64 mod p (into the Montgomery domain)
 };
 
+// release / acquire of a step-done flag at GPU scope (the build kernel runs
+// beside the steps kernel and follows it step by step)
+__device__ __forceinline__ void flag_release(uint32_t* f, uint32_t v) {
+  // after a CTA barrier: the release is cumulative over the other threads' writes
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(f), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t flag_acquire(const uint32_t* f) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(f) : "memory");
+  return v;
+}
+
 // (a*w + (p-b)*y) * 2^-32 mod p, all inputs < p, result < p
 __device__ __forceinline__ uint32_t redc_axby(uint32_t a, uint32_t w, uint32_t b, uint32_t y,
                                               const F31& f) {
@@ -109,7 +121,7 @@ __device__ __forceinline__ uint32_t redc3(uint32_t d, uint32_t v, uint32_t al, u
 template <int NC>
 __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int* klist,
                             uint32_t* pbuf, const F31& f, uint32_t* Ct, uint32_t* recC,
-                            unsigned long long* trace) {
+                            unsigned long long* trace, uint32_t* sig, uint32_t epoch) {
   static_assert(NC == 32, "16 threads x 4 columns per row, 64 columns");
   static_assert(((NC / 2 - 1) & 1) == 1, "the last block uses pivot buffer 1");
   const int tid = threadIdx.x, gi = tid >> 4, gs = tid & 15;
@@ -179,6 +191,10 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
     uint32_t dq = pbuf[tid];
     if (NC > 16 && tid < 16) dq = redc_mul(dq, S, f);  // the skipped rescalings
     pbuf[64 + tid] = invmod(dq, f);
+  } else if (sig && tid == (int)blockDim.x - 1) {
+    // the previous step's done flag: its GPU-scope release (~0.7 us) hides
+    // behind the inversions instead of delaying a barrier
+    flag_release(sig, epoch);
   }
   __syncthreads();
   const uint32_t iq = pbuf[64 + gi];
@@ -348,6 +364,8 @@ struct StepArgs {
   int fold_k;         // products between folds (pointwise.cu fold_period)
   F31 f;
   unsigned long long* trace;  // profiling only (FPM_MBASIS_TRACE): [T][6] clocks
+  uint32_t* flags;    // [T + 1]: flags[k] = epoch once step k's record is written
+  uint32_t epoch;     //          flags[T] = epoch once every output is written
 };
 
 constexpr int kStepThreads = 512;
@@ -357,6 +375,7 @@ constexpr int kStepThreads = 512;
 
 __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __grid_constant__ StepArgs a) {
   pdl_wait();
+  pdl_trigger();  // the build kernel starts now and waits on the step flags
   extern __shared__ __align__(16) unsigned char smraw[];
   const int m = a.m, n = a.n, T = a.T;
   const int tid = threadIdx.x;
@@ -399,6 +418,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   }
   __syncthreads();
 
+  int pending = -1;  // step whose done flag is not released yet
   for (int k = 0; k < T; ++k) {
     const uint32_t* Gk = G + (size_t)k * mn;  // + rowoff[i] - i*n per row
     auto gk = [&](int idx) {
@@ -466,8 +486,10 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
       }
       __syncthreads();
       if (solve_pairs<32>(X, m, ord, klist, sbuf, f, W, a.rec_Ct + (size_t)k * m * m,
-                          a.trace ? a.trace + k * 8 : nullptr)) {
+                          a.trace ? a.trace + k * 8 : nullptr,
+                          pending >= 0 ? a.flags + pending : nullptr, a.epoch)) {
         fast_done = pairs_done = true;
+        pending = -1;
       } else {
         // degenerate residual: the general elimination on W = R_k from X = I
         __syncthreads();
@@ -644,7 +666,14 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     for (int q = tid; q < np; q += kStepThreads) a.rec_plist[(size_t)k * m + q] = plist[q];
     __syncthreads();
     const int nk = s_nk;
-    if (np == 0) continue;  // R = 0: nothing changes (appint.py:171)
+    if (np == 0) {  // R = 0: nothing changes (appint.py:171)
+      if (tid == 0) {
+        if (pending >= 0) flag_release(a.flags + pending, a.epoch);
+        flag_release(a.flags + k, a.epoch);
+      }
+      pending = -1;
+      continue;
+    }
     uint32_t* Ct = W;  // compact [np][nk]
     uint32_t* recC = a.rec_Ct + (size_t)k * m * m;
     if (pairs_done) {
@@ -671,6 +700,16 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     }
     __syncthreads();
     STEP_TRACE(2);
+    // step k's record is complete.  A GPU-scope release costs ~0.7 us on the
+    // thread that issues it, so the flag of every step but the last is left
+    // pending and released from an idle thread inside the next step's solve
+    // (the build kernel only needs to keep up, not to be early)
+    if (pending >= 0 && tid == 0) flag_release(a.flags + pending, a.epoch);
+    pending = k;
+    if (k == T - 1) {
+      if (tid == 0) flag_release(a.flags + k, a.epoch);
+      pending = -1;
+    }
 
     // ---- residual list: kernel rows G[t][i] += sum_q Ct G[t][plist[q]], t > k -
     for (int q = tid; q < np; q += kStepThreads) prow[q] = rowoff[plist[q]];
@@ -786,6 +825,8 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
     STEP_TRACE(4);
   }
   for (int i = tid; i < m; i += kStepThreads) a.sft_out[i] = sft[i];
+  __syncthreads();
+  if (tid == 0) flag_release(a.flags + T, a.epoch);
 }
 
 struct BuildArgs {
@@ -798,16 +839,22 @@ struct BuildArgs {
   int fold_k;
   F31 f;
   const uint32_t* alpha;  // interpolants: pivot rows times (x - alpha_k)
+  const uint32_t* flags;  // step-done flags of the steps kernel (see StepArgs)
+  uint32_t epoch;
 };
 
-// one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j.  Every step's
-// record (pivot list, compact Ct) is staged into shared memory up front with
-// cp.async (all loads in flight) and the per-step row maps are built in
-// parallel; a step then gathers the pivot rows' coefficients (and shifts
-// them by x) and computes the kernel rows P1[t][klist[kr]] = P0[t][klist[kr]]
+// one CTA per column j of P: apply Q_0 .. Q_{T-1} to e_j.  Step k's record
+// (pivot list, compact Ct) is staged into shared memory when its flag is set;
+// the step then gathers the pivot rows' coefficients (and shifts them by x)
+// and computes the kernel rows P1[t][klist[kr]] = P0[t][klist[kr]]
 // + sum_q Ct[q][kr] P0[t][plist[q]] with independent shared loads.
 __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
-  pdl_wait();
+  // no pdl_wait: launched as the programmatic dependent of the steps kernel
+  // (which triggers right after its own wait), this kernel runs BESIDE it and
+  // applies step k as soon as flags[k] says its record is written; only the
+  // last step's update is left when the steps kernel ends.  Records are read
+  // with ld.global.cg: the buffers are reused leaf after leaf, and L1 may
+  // hold an earlier leaf's lines.
   extern __shared__ __align__(16) uint32_t bsm[];
   const int m = a.m, T = a.T, j = blockIdx.x;
   const int tid = threadIdx.x, NT = blockDim.x;
@@ -816,58 +863,40 @@ __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
   uint32_t* P0 = bsm;                                     // [L1][m]
   uint32_t* P1 = P0 + (size_t)L1 * m;                     // [L1][m]
   uint32_t* Pp = P1 + (size_t)L1 * m;                     // [L1][m] gathered pivot rows
-  uint32_t* Cs = Pp + (size_t)L1 * m;                     // [T][cmax] compact Ct
-  int* nps = (int*)(Cs + (size_t)T * cmax);               // [T]
-  short* plist = (short*)(nps + T);                       // [T][m]
-  short* klist = plist + (size_t)T * m;                   // [T][m]
-  short* isp = klist + (size_t)T * m;                     // [T][m]: pivot flag
-  {
-    const uint32_t base = (uint32_t)__cvta_generic_to_shared(Cs);
-    for (int k = 0; k < T; ++k) {
-      const int cnt = a.rec_np[k] * (m - a.rec_np[k]);
-      for (int c = tid; c < cnt; c += NT)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
-                         base + 4u * (uint32_t)(k * cmax + c)),
-                     "l"(a.rec_Ct + (size_t)k * m * m + c));
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  }
-  for (int k = tid; k < T; k += NT) nps[k] = a.rec_np[k];
-  for (int idx = tid; idx < T * m; idx += NT) {
-    plist[idx] = (short)a.rec_plist[idx];
-    isp[idx] = 0;
-  }
+  uint32_t* Cs = Pp + (size_t)L1 * m;                     // [cmax] compact Ct of the step
+  short* pl = (short*)(Cs + cmax);                        // [m] pivot rows
+  short* kl = pl + m;                                     // [m] kernel rows in index order
+  short* isp = kl + m;                                    // [m] pivot flag
   for (int idx = tid; idx < L1 * m; idx += NT) P0[idx] = (idx == j) ? 1u : 0u;
-  __syncthreads();
-  for (int idx = tid; idx < T * m; idx += NT) {
-    const int k = idx / m, q = idx - (idx / m) * m;
-    if (q < nps[k]) isp[k * m + plist[idx]] = 1;
-  }
-  __syncthreads();
-  {  // kernel rows in index order: ballot prefix, one warp per step
-    const int w = tid >> 5, lane = tid & 31;
-    for (int k = w; k < T; k += NT / 32) {
-      int base = 0;
-      for (int i0 = 0; i0 < m; i0 += 32) {
-        const int i = i0 + lane;
-        const bool kr = i < m && !isp[k * m + i];
-        const unsigned bal = __ballot_sync(0xffffffffu, kr);
-        if (kr) klist[k * m + base + __popc(bal & ((1u << lane) - 1u))] = (short)i;
-        base += __popc(bal);
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-  __syncthreads();
   const bool k4 = a.fold_k >= 4;
   int L = 1;
   for (int k = 0; k < T; ++k) {
-    const int np = nps[k];
+    if (tid == 0)
+      while (flag_acquire(a.flags + k) != a.epoch) __nanosleep(64);
+    __syncthreads();  // also: the previous step's reads of Cs / pl / kl are done
+    const int np = __ldcg(a.rec_np + k);
     if (np == 0) continue;  // R = 0: the reference leaves P unchanged
     const int nk = m - np;
-    const uint32_t* Ct = Cs + (size_t)k * cmax;
-    const short* pl = plist + k * m;
-    const short* kl = klist + k * m;
+    for (int i = tid; i < m; i += NT) isp[i] = 0;
+    for (int c = tid; c < np * nk; c += NT) Cs[c] = __ldcg(a.rec_Ct + (size_t)k * m * m + c);
+    __syncthreads();
+    for (int q = tid; q < np; q += NT) {
+      const int i = __ldcg(a.rec_plist + (size_t)k * m + q);
+      pl[q] = (short)i;
+      isp[i] = 1;
+    }
+    __syncthreads();
+    if (tid < 32) {  // kernel rows in index order: ballot prefix
+      int base = 0;
+      for (int i0 = 0; i0 < m; i0 += 32) {
+        const int i = i0 + tid;
+        const bool kr = i < m && !isp[i];
+        const unsigned bal = __ballot_sync(0xffffffffu, kr);
+        if (kr) kl[base + __popc(bal & ((1u << tid) - 1u))] = (short)i;
+        base += __popc(bal);
+      }
+    }
+    const uint32_t* Ct = Cs;
     // pivot rows: gather (t < L) and shift by x into P1 (t = 0 .. L)
     for (int idx = tid; idx < (L + 1) * np; idx += NT) {
       const int t = idx / np, q = idx - (idx / np) * np;
@@ -912,6 +941,11 @@ __global__ void __launch_bounds__(256) mbasis_build_kernel(BuildArgs a) {
     uint32_t* tmp = P0; P0 = P1; P1 = tmp;
     ++L;
   }
+  // every output of the steps kernel (the final shift) is written: this
+  // kernel's completion then orders the whole leaf before its successors
+  if (tid == 0)
+    while (flag_acquire(a.flags + T) != a.epoch) __nanosleep(64);
+  __syncthreads();
   // column j of P, entry-major: P[(i*m + j)*ps + t]
   const int ps = (int)a.ps;
   for (int idx = tid; idx < m * ps; idx += NT) {
@@ -943,11 +977,10 @@ size_t steps_smem(int m, int n, int T) {
 
 int fold_period(uint32_t p);  // pointwise.cu
 
-// mbasis_build_kernel: two P buffers, the compact records, row maps
+// mbasis_build_kernel: three P buffers, one step's compact record and row maps
 size_t build_smem(int m, int order) {
   const size_t cmax = (size_t)(m / 2) * ((m + 1) / 2);
-  return 3 * (size_t)(order + 1) * m * 4 + (size_t)order * cmax * 4 + (size_t)order * 4 +
-         (size_t)order * m * 6 + 16;
+  return 3 * (size_t)(order + 1) * m * 4 + cmax * 4 + (size_t)m * 6 + 16;
 }
 
 int mbasis_fast_max_order(int m, int n) {
@@ -982,6 +1015,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   sa.m = m; sa.n = n; sa.T = order; sa.s = s_dev;
   sa.rec_np = rec_np; sa.rec_plist = rec_plist; sa.rec_Ct = rec_Ct;
   sa.sft_out = sft_dev; sa.fold_k = K; sa.f = f;
+  FPM_TRY(cx.leaf_flags(&sa.flags, &sa.epoch));
 #ifdef FPM_TRACE
   // profiling build only (tools/mbasis_trace.py)
   if (std::getenv("FPM_MBASIS_TRACE")) {
@@ -1004,6 +1038,7 @@ int mbasis_fast(Context& cx, uint32_t p, const void* F, int m, int n, long long 
   ba.rec_np = rec_np; ba.rec_plist = rec_plist; ba.rec_Ct = rec_Ct; ba.m = m; ba.T = order;
   ba.alpha = alpha_dev;
   ba.P = (uint32_t*)P; ba.ps = ps; ba.fold_k = K; ba.f = f;
+  ba.flags = sa.flags; ba.epoch = sa.epoch;
   const size_t bsmem = build_smem(m, order);
   static size_t battr = 0;
   if (bsmem > 48 * 1024 && bsmem > battr) {

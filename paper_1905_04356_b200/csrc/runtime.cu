@@ -173,10 +173,23 @@ Context::~Context() {
       cudaFree(t);
   }
   if (pinned_) cudaFreeHost(pinned_);
+  if (leaf_flags_) cudaFree(leaf_flags_);
   for (auto& a : aux_)
     if (a) cudaStreamDestroy(a);
   for (auto e : ev_pool_) cudaEventDestroy(e);
   if (own_stream_ && stream_) cudaStreamDestroy(stream_);
+}
+
+int Context::leaf_flags(uint32_t** flags, uint32_t* epoch) {
+  std::lock_guard<std::mutex> lk(mu_);
+  if (!leaf_flags_) {
+    FPM_CUDA_TRY(cudaMalloc(&leaf_flags_, 128 * sizeof(uint32_t)));
+    FPM_CUDA_TRY(cudaMemset(leaf_flags_, 0, 128 * sizeof(uint32_t)));
+  }
+  if (++leaf_epoch_ == 0) ++leaf_epoch_;  // 0 is the cleared state
+  *flags = leaf_flags_;
+  *epoch = leaf_epoch_;
+  return kOk;
 }
 
 int Context::set_stream(cudaStream_t s) {

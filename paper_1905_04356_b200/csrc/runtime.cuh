@@ -61,6 +61,10 @@ class Context {
   cudaEvent_t take_event();
   void give_event(cudaEvent_t e);
   int prime_const(uint32_t p, int logn, PrimeConst* out);
+  // PM-Basis leaf (mbasis_fast.cu): the step-done flags through which the
+  // build kernel follows the running steps kernel, and a fresh epoch (the
+  // value a flag takes when its step of THIS leaf is recorded)
+  int leaf_flags(uint32_t** flags, uint32_t* epoch);
 
   // stage profiling (tracing subsystem): CUDA events around each kernel
   // stage on the context stream, read back by fpm_profile_get
@@ -91,6 +95,8 @@ class Context {
   std::map<std::pair<uint32_t, int>, BigPlan> big_plans_;
   void* pinned_ = nullptr;
   size_t pinned_bytes_ = 0;
+  uint32_t* leaf_flags_ = nullptr;
+  uint32_t leaf_epoch_ = 0;
 };
 
 // RAII stage timer: no-op unless the context is profiling
