@@ -96,6 +96,11 @@ void mma64_ntt_tables(uint32_t p, uint32_t omega, std::vector<uint8_t>* out) {
 
 namespace {
 
+#ifndef FPM_M64_VARIANT
+#define FPM_M64_VARIANT 15  // measured on cfg5: 0 -> 3.28 ms per product, 14 / 15 -> 3.205
+#endif
+constexpr bool kP1MH = (FPM_M64_VARIANT & 1) != 0, kP1ML = (FPM_M64_VARIANT & 2) != 0;
+constexpr bool kP2MH = (FPM_M64_VARIANT & 4) != 0, kP2ML = (FPM_M64_VARIANT & 8) != 0;
 constexpr int kWorkers = 16;                     // worker warps (warps 1 .. 16)
 constexpr int kLoaders = 2;                      // input warps (after the store warp)
 constexpr int kThreads = 32 * (2 + kWorkers + kLoaders);
@@ -120,6 +125,7 @@ struct Mma64Args {
   long long tiles1, tiles;
   uint32_t p, w16s, pinv;            // w16s = floor(2^48 / p), pinv = p^-1 mod 2^32
   uint32_t negp, zero;               // 2^32 - p; 0 (opaque: keeps 3-input adds on the ALU pipe)
+  uint32_t c256;                     // 256 (opaque: keeps d * 256 + e one IMAD)
   const uint8_t* tab;
   int tma_out;                       // point-major output by TMA stores
   int dbg;                           // timing experiments (option ntt_mma_dbg): 1 = no input loads
@@ -133,13 +139,6 @@ __device__ __forceinline__ void sts128(uint32_t addr, uint32_t x, uint32_t y, ui
 }
 __device__ __forceinline__ void sts32(uint32_t addr, uint32_t x) {
   asm volatile("st.shared.b32 [%0], %1;\n" ::"r"(addr), "r"(x) : "memory");
-}
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-  uint4 v;
-  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];\n"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "r"(addr));
-  return v;
 }
 // 4-D TMA tensor store shared -> global (bulk group)
 __device__ __forceinline__ void tma_store_4d(const void* tmap, uint32_t src, int c0, int c1, int c2,
@@ -173,14 +172,18 @@ __device__ __forceinline__ uint32_t prmt0(uint32_t a, uint32_t sel) {
 // (L - p if L >= p), so L + r < 2^32 - 2^24 - p + p.
 // z = 0 at run time: a 3-input add is an ALU IADD3, where ptxas would issue a
 // 2-input one as IMAD.IADD on the multiply pipe that the epilogue saturates.
-template <bool RL>
+// MH / ML: form H / L with one IMAD by c256 (= 256, opaque so that it stays a
+// multiply on the FMA pipe) instead of a byte permute and an add on the ALU
+// pipe -- the pass picks the split that balances its two pipes.
+template <bool RL, bool MH, bool ML>
 __device__ __forceinline__ uint32_t fold4w(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
-                                           uint32_t p, uint32_t negp, uint32_t w16s, uint32_t z) {
-  const uint32_t H = d2 + prmt0(d3, 0x2104) + z;        // d2 + (d3 << 8)
+                                           uint32_t p, uint32_t negp, uint32_t w16s, uint32_t z,
+                                           uint32_t c256) {
+  const uint32_t H = MH ? d3 * c256 + d2 : d2 + prmt0(d3, 0x2104) + z;  // d2 + (d3 << 8)
   const uint32_t q = __umulhi(H, w16s);
   uint32_t r = prmt0(H, 0x1044) + q * negp;             // (H << 16) - q p, in [0, 2p)
   r = min(r, r - p);
-  uint32_t L = d0 + prmt0(d1, 0x2104) + z;              // d0 + (d1 << 8)
+  uint32_t L = ML ? d1 * c256 + d0 : d0 + prmt0(d1, 0x2104) + z;        // d0 + (d1 << 8)
   if (RL) L = min(L, L - p);  // !RL: the planes are < 2^23 (K' = 128), L < 2^31 + 2^23
   return L + r + z;
 }
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int t = R & 7, lq = lane >> 3;  // transform of the tile; row digit = 4 q + lq
     const uint32_t tl = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(64 * h);
     const uint32_t p = a.p, w16s = a.w16s, negp = a.negp, pinv = a.pinv, z = a.zero;
+    const uint32_t c256 = a.c256;
     // P1 -> P2 operand: value (a = 16 s + 4 q + lq, column j = 16 h + 8 g + i)
     // -> slice s, operand K(j) & 3 = g + 2 (h >> 1), row group K(j) >> 2 =
     // (h & 1) + 2 brev3(i), K chunk q, word lq
@@ -501,10 +505,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int i = 0; i < 4; ++i)
                 y[4 * hq + i] = (pass == 0 && kHalfK)
-                                    ? fold4w<false>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
-                                                    v[4 * i + 3], p, negp, w16s, z)
-                                    : fold4w<true>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
-                                                   v[4 * i + 3], p, negp, w16s, z);
+                                    ? fold4w<false, kP1MH, kP1ML>(v[4 * i], v[4 * i + 1],
+                                                                  v[4 * i + 2], v[4 * i + 3], p,
+                                                                  negp, w16s, z, c256)
+                                : pass == 0
+                                    ? fold4w<true, kP1MH, kP1ML>(v[4 * i], v[4 * i + 1],
+                                                                 v[4 * i + 2], v[4 * i + 3], p,
+                                                                 negp, w16s, z, c256)
+                                    : fold4w<true, kP2MH, kP2ML>(v[4 * i], v[4 * i + 1],
+                                                                 v[4 * i + 2], v[4 * i + 3], p,
+                                                                 negp, w16s, z, c256);
               if (g == 0) {
                 // refill this buffer with the matching quarter of the second half
                 if (hq == 0) {
@@ -623,6 +633,7 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   a.pinv = inv;
   a.negp = 0u - a.p;
   a.zero = 0;
+  a.c256 = 256;
   a.dbg = (int)option(kOptNttMmaDbg);
   a.tab = ps.pr[0].mma + kMma64TabOff;
   static bool attr = false;
