@@ -166,26 +166,23 @@ __device__ __forceinline__ uint32_t prmt0(uint32_t a, uint32_t sel) {
   return r;
 }
 
-// sum_r 2^(8r) d[r] (d0..d2 <= 256 * 255^2, d3 < 2^23) -> a congruent word
-// < 2^32:  H = d2 + 2^8 d3 < 2^32, H 2^16 mod p by Shoup then reduced to
-// [0, p);  L = d0 + 2^8 d1 <= 257 * 256 * 255^2 < 2^32 - 2^24 reduced once
-// (L - p if L >= p), so L + r < 2^32 - 2^24 - p + p.
-// z = 0 at run time: a 3-input add is an ALU IADD3, where ptxas would issue a
-// 2-input one as IMAD.IADD on the multiply pipe that the epilogue saturates.
+// V = sum_r 2^(8r) d[r] (d0..d2 <= 256 * 255^2, d3 < 2^23) -> a congruent word
+// < 2p + 2^16 with ONE multiply-high: L = d0 + 2^8 d1 <= 257 * 256 * 255^2 <
+// 2^32 and H = d2 + 2^8 d3 < 2^24 + 2^31 are exact, V = L + 2^16 H = 2^16 Hs +
+// (L mod 2^16) with Hs = H + floor(L / 2^16) < 2^32; q = hi(Hs floor(2^48 / p))
+// is the Shoup quotient of Hs 2^16, so 0 <= 2^16 Hs - q p < 2p and
+// V - q p = L + (H << 16) - q p (mod 2^32) < 2p + 2^16 < 2^32.
 // MH / ML: form H / L with one IMAD by c256 (= 256, opaque so that it stays a
-// multiply on the FMA pipe) instead of a byte permute and an add on the ALU
-// pipe -- the pass picks the split that balances its two pipes.
-template <bool RL, bool MH, bool ML>
+// multiply on the FMA pipe) instead of a byte permute and a 3-input add (z = 0,
+// opaque: a 2-input add would be issued as IMAD.IADD) on the ALU pipe.
+template <bool MH, bool ML>
 __device__ __forceinline__ uint32_t fold4w(uint32_t d0, uint32_t d1, uint32_t d2, uint32_t d3,
-                                           uint32_t p, uint32_t negp, uint32_t w16s, uint32_t z,
+                                           uint32_t negp, uint32_t w16s, uint32_t z,
                                            uint32_t c256) {
   const uint32_t H = MH ? d3 * c256 + d2 : d2 + prmt0(d3, 0x2104) + z;  // d2 + (d3 << 8)
-  const uint32_t q = __umulhi(H, w16s);
-  uint32_t r = prmt0(H, 0x1044) + q * negp;             // (H << 16) - q p, in [0, 2p)
-  r = min(r, r - p);
-  uint32_t L = ML ? d1 * c256 + d0 : d0 + prmt0(d1, 0x2104) + z;        // d0 + (d1 << 8)
-  if (RL) L = min(L, L - p);  // !RL: the planes are < 2^23 (K' = 128), L < 2^31 + 2^23
-  return L + r + z;
+  const uint32_t L = ML ? d1 * c256 + d0 : d0 + prmt0(d1, 0x2104) + z;  // d0 + (d1 << 8)
+  const uint32_t q = __umulhi(H + (L >> 16), w16s);
+  return (L + (H << 16)) + q * negp;
 }
 // Montgomery product y W 2^-32 mod p (y < 2^32, W < p) in (0, 2p)
 __device__ __forceinline__ uint32_t mont(uint32_t y, uint32_t W, uint32_t p, uint32_t pinv) {
@@ -263,7 +260,6 @@ __host__ __device__ constexpr int brev3c(int x) {
   return ((x & 1) << 2) | (x & 2) | ((x >> 2) & 1);
 }
 
-template <bool kHalfK>  // P1 reads only the inputs b < 32 (len <= 2048): K' = 128
 __global__ void __launch_bounds__(kThreads, 1)
     ntt_mma64_kernel(const __grid_constant__ Mma64Args a, const __grid_constant__ CUtensorMap om1,
                      const __grid_constant__ CUtensorMap om2) {
@@ -501,20 +497,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int hq = 0; hq < 2; ++hq) {
               const uint32_t(&v)[16] = hq == 0 ? va : vb;
-              // P1 with K' = 128: D_r < 2^23, so d0 + 2^8 d1 + r < 2^31 + 2^23 + p
 #pragma unroll
               for (int i = 0; i < 4; ++i)
-                y[4 * hq + i] = (pass == 0 && kHalfK)
-                                    ? fold4w<false, kP1MH, kP1ML>(v[4 * i], v[4 * i + 1],
-                                                                  v[4 * i + 2], v[4 * i + 3], p,
-                                                                  negp, w16s, z, c256)
-                                : pass == 0
-                                    ? fold4w<true, kP1MH, kP1ML>(v[4 * i], v[4 * i + 1],
-                                                                 v[4 * i + 2], v[4 * i + 3], p,
-                                                                 negp, w16s, z, c256)
-                                    : fold4w<true, kP2MH, kP2ML>(v[4 * i], v[4 * i + 1],
-                                                                 v[4 * i + 2], v[4 * i + 3], p,
-                                                                 negp, w16s, z, c256);
+                y[4 * hq + i] =
+                    pass == 0 ? fold4w<kP1MH, kP1ML>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                                                     v[4 * i + 3], negp, w16s, z, c256)
+                              : fold4w<kP2MH, kP2ML>(v[4 * i], v[4 * i + 1], v[4 * i + 2],
+                                                     v[4 * i + 3], negp, w16s, z, c256);
               if (g == 0) {
                 // refill this buffer with the matching quarter of the second half
                 if (hq == 0) {
@@ -638,10 +627,8 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   a.tab = ps.pr[0].mma + kMma64TabOff;
   static bool attr = false;
   if (!attr) {
-    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel<true>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel<false>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    FPM_CUDA_TRY(cudaFuncSetAttribute(ntt_mma64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmem));
     attr = true;
   }
   CUtensorMap om1{}, om2{};
@@ -652,12 +639,8 @@ int launch_ntt_fwd_mma64(const NttFwdArgs& f, const PrimeSet& ps, cudaStream_t s
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long grid = a.tiles < sms ? a.tiles : sms;
-  if (a.kc1 == 8)
-    FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel<true>, dim3((unsigned)grid), dim3(kThreads), kSmem, st,
-                            a, om1, om2));
-  else
-    FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel<false>, dim3((unsigned)grid), dim3(kThreads), kSmem,
-                            st, a, om1, om2));
+  FPM_CUDA_TRY(launch_pdl(ntt_mma64_kernel, dim3((unsigned)grid), dim3(kThreads), kSmem, st, a,
+                          om1, om2));
   FPM_LAUNCH_CHECK();
   return kOk;
 }
