@@ -109,8 +109,9 @@ class Clocks:
             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=2.0):
         self.index = index
+        self.period = period_ms * 1e-3
         self.samples = []
         self.reasons = set()
         self.max_mhz = None
@@ -143,7 +144,7 @@ class Clocks:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            time.sleep(self.period)
 
     def stop(self):
         if not self.ok:
@@ -154,7 +155,7 @@ class Clocks:
         sm = sorted(self.samples)
         med = sm[len(sm) // 2] if sm else None
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(sm), "source": "NVML (nvidia_ml_py), 2 ms period"}
+                "samples": len(sm), "source": f"NVML (nvidia_ml_py), {self.period * 1e3:g} ms period"}
 
 
 def read_peaks():
@@ -687,6 +688,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg5", choices=sorted(CONFIGS))
+    ap.add_argument("--clock-period-ms", type=float, default=2.0,
+                    help="NVML clock / throttle-reason sampling period during the timed steps")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip cpu_baseline / e2e / per-config table")
     args = ap.parse_args()
@@ -730,7 +733,7 @@ def main():
         def step(cfg_, inp, out):
             return pm_mul_prime_split(inp[0], inp[1], cfg_["p"], dst=0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)  # > 126 MB L2
-    clocks = Clocks(local)
+    clocks = Clocks(local, args.clock_period_ms)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
