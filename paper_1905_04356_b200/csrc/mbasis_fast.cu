@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdlib>
 #include "pmbasis.cuh"
+#include "tc_common.cuh"
 
 namespace fpm {
 namespace {
@@ -118,12 +119,19 @@ __device__ __forceinline__ uint32_t redc3(uint32_t d, uint32_t v, uint32_t al, u
 // Thread (gi, gs) holds row gi, columns gs + 16u.  W is R_k with row stride
 // NC + 1 (conflict-free column reads).  Returns false (uniformly) on a zero
 // leading minor; the shared step state is then untouched.
+//
+// No CTA barrier per block: rows c, c+1 live in warp c / 2, which publishes
+// them in the block's OWN buffer (NC / 2 buffers of 128 words) when it gets to
+// block c -- it has applied every earlier block by then -- and arrives on the
+// block's mbarrier bars[c / 2] (phase parity par of this call); the other
+// warps wait on it, suspended, and each runs ahead as far as its data allows
+// (a barrier per block cost as much as the block's arithmetic).
 template <int NC>
 __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int* klist,
                             uint32_t* pbuf, const F31& f, uint32_t* Ct, uint32_t* recC,
-                            unsigned long long* trace, uint32_t* sig, uint32_t epoch) {
+                            unsigned long long* trace, uint32_t* sig, uint32_t epoch,
+                            uint64_t* bars, uint32_t par) {
   static_assert(NC == 32, "16 threads x 4 columns per row, 64 columns");
-  static_assert(((NC / 2 - 1) & 1) == 1, "the last block uses pivot buffer 1");
   const int tid = threadIdx.x, gi = tid >> 4, gs = tid & 15;
   const int nk = m - NC;
   uint32_t v[4];
@@ -142,15 +150,14 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
   for (int c = 0; c < NC; c += 2) {
     constexpr int kSkip = 16;
     const int u0 = c >= kSkip ? 1 : 0;
-    uint32_t* pb = pbuf + ((c >> 1) & 1) * 128;
-    if (gi == c) {
+    uint32_t* pb = pbuf + (c >> 1) * 128;
+    if ((tid >> 5) == (c >> 1)) {  // the warp of rows c, c + 1
 #pragma unroll
-      for (int u = 0; u < 4; ++u) pb[gs + 16 * u] = v[u];
-    } else if (gi == c + 1) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) pb[64 + gs + 16 * u] = v[u];
+      for (int u = 0; u < 4; ++u) pb[(gi - c) * 64 + gs + 16 * u] = v[u];
+      __syncwarp();
+      if ((tid & 31) == 0) tc::mbar_arrive(&bars[c >> 1]);
     }
-    __syncthreads();
+    tc::mbar_wait(&bars[c >> 1], par);
     const uint32_t a = pb[c], b = pb[c + 1], d = pb[64 + c], e = pb[64 + c + 1];
     const uint32_t dl = redc_axby(a, e, b, d, f);
     if (a == 0 || dl == 0) return false;  // every thread read the same block
@@ -182,9 +189,13 @@ __device__ bool solve_pairs(const uint32_t* W, int m, const int* ord, const int*
     }
   }
   if (trace && tid == 0) trace[6] = clock64();
-  // d_q = M[q][q] (row q: lane q & 15, register q >> 4) is published in the
-  // pivot buffer the last block did not use; one warp inverts all NC of them
-  // (16 lanes per row inverting the same value cost 4x the issue slots)
+  // d_q = M[q][q] (row q: lane q & 15, register q >> 4) is published in
+  // block 0's pivot buffer (every warp is past it: each waited for the last
+  // block, whose rows were published by a warp that had read all the others'
+  // -- but a warp may still be reading the LAST block's buffer, hence the CTA
+  // barrier first); one warp inverts all NC of them (16 lanes per row
+  // inverting the same value cost 4x the issue slots)
+  __syncthreads();
   if (gs == (gi & 15)) pbuf[gi] = (gi >> 4) ? v[1] : v[0];
   __syncthreads();
   if (tid < NC) {
@@ -402,7 +413,15 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   long long* krow = prow + m;                     // m: rowoff[klist[kr]] of the step
   __shared__ int s_key[2];
   __shared__ int s_nk;
-  __shared__ uint32_t sbuf[2 * 128];  // block solves: pivot rows (+ column), double buffered
+  // block solves: pivot rows (+ column); solve_pairs: one 128-word buffer and
+  // one mbarrier per 2 x 2 block
+  __shared__ uint32_t sbuf[16 * 128];
+  __shared__ uint64_t sbar[16];
+  uint32_t spar = 0;  // phase parity of sbar for the next solve_pairs call
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < 16; ++b) tc::mbar_init(&sbar[b], 1);
+    tc::fence_mbar_init();
+  }
 
   const int hw = tid >> 4, l16 = tid & 15;  // half-warp per row
   constexpr int kRowsPerPass = kStepThreads / 16;
@@ -487,12 +506,18 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
       __syncthreads();
       if (solve_pairs<32>(X, m, ord, klist, sbuf, f, W, a.rec_Ct + (size_t)k * m * m,
                           a.trace ? a.trace + k * 8 : nullptr,
-                          pending >= 0 ? a.flags + pending : nullptr, a.epoch)) {
+                          pending >= 0 ? a.flags + pending : nullptr, a.epoch, sbar, spar)) {
         fast_done = pairs_done = true;
         pending = -1;
+        spar ^= 1u;
       } else {
         // degenerate residual: the general elimination on W = R_k from X = I
         __syncthreads();
+        if (tid == 0) {  // only the blocks before the zero minor completed a phase
+          for (int b = 0; b < 16; ++b) tc::mbar_init(&sbar[b], 1);
+          tc::fence_mbar_init();
+        }
+        spar = 0;
         for (int idx = tid; idx < (int)mn; idx += kStepThreads) W[idx] = gk(idx);
         for (int i = tid; i < m; i += kStepThreads) piv[i] = 0;
         for (int idx = tid; idx < m * m; idx += kStepThreads)

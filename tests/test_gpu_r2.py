@@ -114,3 +114,38 @@ def test_2d_blocks_on_nccl():
         Cb = parallel.pm_mul_2d(Ad, Bd, p, r, 8)
         (a, b), (c, d) = parallel.block_of(r, 8, 40, 24)
         assert np.array_equal(dense.to_numpy(Cb, p), want[a:b, c:d])
+
+
+def _degenerate_64x32(kind, order, seed):
+    """64 x 32 inputs whose residuals have zero leading minors: the pair solve
+    of the leaf (csrc/mbasis_fast.cu:solve_pairs) must hand over to the general
+    elimination, as appint._mbasis1_struct (appint.py:24-60) picks other pivots"""
+    p = 2013265921
+    rng = np.random.default_rng(seed)
+    Fm = rng.integers(0, p, size=(64, 32, order), dtype=np.uint64)
+    if kind == "equal_rows":
+        Fm[1] = Fm[0]
+        Fm[40] = Fm[7]
+    elif kind == "zero_column":
+        Fm[:, 5, :] = 0
+    elif kind == "zero_constant":
+        Fm[:, :, 0] = 0          # first residual is zero: a step without pivots
+    elif kind == "zero_rows":
+        Fm[0:3] = 0
+    elif kind == "rank_drop":
+        Fm[:, 16:, :] = Fm[:, :16, :]   # column j + 16 repeats column j
+    return p, Fm
+
+
+@pytest.mark.parametrize("kind", ["equal_rows", "zero_column", "zero_constant", "zero_rows",
+                                  "rank_drop"])
+@pytest.mark.parametrize("order,shift", [(8, "uniform"), (16, "mixed")])
+def test_leaf_pair_solve_degenerate_residuals(kind, order, shift):
+    from oracle import oracle as O
+
+    p, Fm = _degenerate_64x32(kind, order, 5)
+    s = [0] * 64 if shift == "uniform" else [(3 * i) % 5 - 2 for i in range(64)]
+    P, _ = dense.pmbasis_dense(dense.to_device(Fm, p), order, s, p)
+    got = dense.to_numpy(P, p).astype(np.uint64)
+    ref = O.pmbasis(p, Fm, order, s)
+    assert got.shape == ref.shape and np.array_equal(got, ref)
