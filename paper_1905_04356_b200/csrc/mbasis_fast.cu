@@ -38,6 +38,8 @@ struct F31 {
   uint64_t mu;       // floor(2^64 / p)
   uint32_t c32;      // 2^32 mod p
   uint32_t r2;       // 2^64 mod p (into the Montgomery domain)
+  uint32_t m58;      // floor(2^58 / p): d_red56 of the residual-list sums
+  uint32_t w24s;     // floor(2^56 / p): Shoup companion of 2^24 (byte-plane scalings)
 };
 
 // release / acquire of a step-done flag at GPU scope (the build kernel runs
@@ -289,7 +291,7 @@ __device__ __forceinline__ void residual_tiles(uint32_t* G, const uint32_t* Ct,
 // fragments are the raw residual words themselves, the B fragments (one kr
 // tile per warp, all four planes, 32 registers) are built once per step in
 // Apk (4 planes x 32 x 32 words, XOR-swizzled rows) and stay in registers.
-// D_r < 128 * 255^2 < 2^23, so sum_r 2^(8r) D_r + G < 2^49 is one d_red64.
+// D_r < 128 * 255^2 < 2^23, so sum_r 2^(8r) D_r + G < 2^49 is one d_red56.
 __device__ __forceinline__ int apk_idx(int r, int row, int q) {
   return (r * 32 + row) * 32 + (q ^ ((row & 7) << 2));
 }
@@ -304,13 +306,26 @@ __device__ __forceinline__ void mma_u8_16832(int (&d)[4], uint32_t a0, uint32_t 
 __device__ void residual_mma(uint32_t* G, const uint32_t* Ct, uint32_t* Apk,
                              const long long* krow, const long long* prow, int k, int nt,
                              size_t mn, const F31& f) {
+  const bool big = f.p >= (1u << 30);  // d_red56 / the shared Shoup quotient need p >= 2^30
   {
-    const uint32_t c8 = 256u % f.p, c16 = (uint32_t)(65536ull % f.p),
-                   c24 = (uint32_t)((1ull << 24) % f.p);
+    // 2^(8b) c mod p for b = 1, 2, 3 from ONE multiply-high (p >= 2^30, c < p):
+    // q3 = hi(c floor(2^56 / p)) is the Shoup quotient of c 2^24 (error < 2),
+    // and q3 >> 8, q3 >> 16 are those of c 2^16, c 2^8 with error < 1.01, so
+    // every c 2^(8b) - q p lies in [0, 2p) -- any such residue is a valid operand
     for (int idx = threadIdx.x; idx < 32 * 32; idx += blockDim.x) {
       const int kr = idx >> 5, q = idx & 31;
       const uint32_t c = Ct[q * 32 + kr];
-      const uint32_t sb[4] = {c, mulmod(c, c8, f), mulmod(c, c16, f), mulmod(c, c24, f)};
+      uint32_t sb[4] = {c, 0u, 0u, 0u};
+      if (big) {
+        const uint32_t q3 = __umulhi(c, f.w24s);
+        sb[1] = (c << 8) - (q3 >> 16) * f.p;
+        sb[2] = (c << 16) - (q3 >> 8) * f.p;
+        sb[3] = (c << 24) - q3 * f.p;
+      } else {
+        sb[1] = mulmod(c, 256u % f.p, f);
+        sb[2] = mulmod(c, (uint32_t)(65536ull % f.p), f);
+        sb[3] = mulmod(c, (uint32_t)((1ull << 24) % f.p), f);
+      }
 #pragma unroll
       for (int r = 0; r < 4; ++r) {  // byte r of sb[0..3] (PRMT)
         const uint32_t lo = __byte_perm(sb[0], sb[1], r | ((4 + r) << 4));
@@ -356,7 +371,7 @@ __device__ void residual_mma(uint32_t* G, const uint32_t* Ct, uint32_t* Apk,
       const uint64_t acc = (uint64_t)(uint32_t)d[0][e] + ((uint64_t)(uint32_t)d[1][e] << 8) +
                            ((uint64_t)(uint32_t)d[2][e] << 16) +
                            ((uint64_t)(uint32_t)d[3][e] << 24) + *dst;
-      *dst = d_red64(acc, f.p, f.mu);
+      *dst = big ? d_red56(acc, f.p, f.m58) : d_red64(acc, f.p, f.mu);
     }
   }
 }
@@ -990,6 +1005,8 @@ F31 make_f31(uint32_t p) {
   f.mu = (uint64_t)((((u128)1) << 64) / p);
   f.c32 = (uint32_t)(((uint64_t)1 << 32) % p);
   f.r2 = (uint32_t)((((u128)1) << 64) % p);
+  f.m58 = p >= (1u << 30) ? (uint32_t)((((uint64_t)1) << 58) / p) : 0u;
+  f.w24s = p >= (1u << 30) ? (uint32_t)((((uint64_t)1) << 56) / p) : 0u;
   return f;
 }
 
