@@ -295,6 +295,26 @@ def test_cfg5_full_size_properties():
         assert np.array_equal(Cn[i:i + 1, j:j + 1], ref)
 
 
+def test_cfg5_full_size_every_entry():
+    """cfg5 at BASELINE's full size, every one of the 256 x 256 x 4095 output
+    words against the multi-threaded C port (oracle/fpm_port.c, itself checked
+    against the pinned oracle in tests/test_oracle_golden.py)."""
+    import torch
+
+    p = P31
+    g = torch.Generator(device="cuda").manual_seed(55)
+    A = torch.randint(0, p, (256, 256, 2048), generator=g, device="cuda", dtype=torch.int64)
+    B = torch.randint(0, p, (256, 256, 2048), generator=g, device="cuda", dtype=torch.int64)
+    A[3, 5, :] = p - 1
+    B[5, 7, :] = p - 1
+    A = A.to(torch.int32)
+    B = B.to(torch.int32)
+    Cn = dense.to_numpy(dense.pm_mul_dense(A, B, p), p)
+    ref = O.port_mul31(p, dense.to_numpy(A, p), dense.to_numpy(B, p))
+    assert Cn.shape == ref.shape
+    assert np.array_equal(Cn.astype(np.uint32), ref)
+
+
 @pytest.mark.parametrize("p", [(1 << 62) - 57, P60, (1 << 40) - 87])
 def test_pm_mul_multiprime_extremes(p):
     """Multi-prime products at the top of the modulus range: the Garner

@@ -90,3 +90,18 @@ def test_pmbasis_sigma64_checksum():
     F = random_polmat_dense(p, 64, 32, 63, rng)
     O.set_threads(8)
     assert O.sha16(p, O.pmbasis(p, F, 64, [0] * 64)) == g["sha16"]
+
+
+@pytest.mark.parametrize("m,k,n,la,lb,threads", [(3, 5, 2, 100, 37, 1), (4, 4, 4, 1024, 1024, 4),
+                                                 (17, 9, 6, 1, 300, 3), (2, 33, 2, 2048, 2047, 2)])
+def test_port_matches_oracle(m, k, n, la, lb, threads):
+    """The multi-threaded C port (oracle/fpm_port.c: the bench's reference arm and
+    the checker of the full-size cfg5 GPU test) against the pinned oracle."""
+    for p in (2013265921, 469762049):
+        rng = np.random.default_rng(m * 1000 + la)
+        A = rng.integers(0, p, size=(m, k, la), dtype=np.uint64)
+        B = rng.integers(0, p, size=(k, n, lb), dtype=np.uint64)
+        A[0, 0, :] = p - 1
+        B[0, 0, :] = p - 1
+        got = O.port_mul31(p, A.astype(np.uint32), B.astype(np.uint32), threads=threads)
+        assert np.array_equal(got.astype(np.uint64), O.pm_mul(p, A, B))
