@@ -394,10 +394,11 @@ int launch_ntt_fwd(int logn, const NttFwdArgs& a_in, const PrimeSet& ps, cudaStr
       return launch_ntt_fwd_persist(logn, a_in, ps, st);
     // generic kernels take one batch at a time
     NttFwdArgs b1 = a_in, b2 = a_in;
-    b1.n_entries2 = 0;
+    b1.n_entries2 = 0; b1.len2 = 0;
     b2.in = a_in.in2; b2.in_stride = a_in.in2_stride; b2.in_prime_stride = a_in.in2_prime_stride;
     b2.n_entries = a_in.n_entries2; b2.out = a_in.out2; b2.out_prime_stride = a_in.out2_prime_stride;
-    b2.n_entries2 = 0;
+    b2.n_entries2 = 0; b2.len2 = 0;
+    if (a_in.len2 > 0) b2.len = a_in.len2;
     FPM_TRY(launch_ntt_fwd(logn, b1, ps, st));
     return launch_ntt_fwd(logn, b2, ps, st);
   }

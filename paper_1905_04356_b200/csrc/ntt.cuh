@@ -44,6 +44,7 @@ struct NttFwdArgs {
   const void* in2;
   long long in2_stride, in2_prime_stride;
   int n_entries2;            // 0: none
+  int len2;                  // coefficients per entry of the second batch (0: len)
   uint32_t* out2;
   long long out2_prime_stride;
   int tma_pm;                // set by the persistent launcher: PM output by TMA stores

@@ -568,6 +568,7 @@ bool aligned16(const void* ptr) { return ((uintptr_t)ptr & 15) == 0; }
 bool ntt_mma_fwd_ok(int logn, const NttFwdArgs& a, const PrimeSet& ps) {
   if (logn != 12 || option(kOptNttNoMma) != 0) return false;
   if (ps.count != 1 || ps.pr[0].mma == nullptr) return false;
+  if (a.len2 > 0 && a.len2 != a.len) return false;  // one length for both batches
   if (ps.pr[0].p <= (1u << 30) || ps.pr[0].p >= (1u << 31)) return false;
   // 32-bit point offsets: 4096 * entries < 2^32
   return a.pm && !a.natural && !a.fold && !a.in64 && !a.reduce && a.len > 0 && a.len <= 4096 &&

@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
   const uint32_t* in2 =
       a.n_entries2 ? (const uint32_t*)a.in2 + (long long)z * a.in2_prime_stride : in1;
   uint32_t* out2 = a.n_entries2 ? a.out2 + (long long)z * a.out2_prime_stride : out1;
-  const bool upper_zero = G::NPASS > 1 && a.len <= G::N / 2;
+  // the two batches may differ in length (A and B of a middle product)
+  const int len1 = a.len, len2 = a.len2 > 0 ? a.len2 : a.len;
   constexpr int FIRST = G::NPASS == 1 ? MAP_LAST : MAP_TOP;
 
   stage_table<LOGN>(tws, pc.tw);
@@ -168,6 +169,8 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     const uint32_t* in = second ? in2 : in1;
     const long long jn = second ? a.n_entries2 : a.n_entries;
     const long long jstride = second ? a.in2_stride : a.in_stride;
+    const int len = second ? len2 : len1;
+    const bool upper_zero = G::NPASS > 1 && len <= G::N / 2;
     if (second) grp -= groups1;
     if (G::TPT >= 32) {
       const long long e = grp * G::TPC + tr;
@@ -176,7 +179,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const int x = xmap<LOGN, FIRST>(lt, i);
-        pre[i] = (valid && x < a.len && !(upper_zero && i >= 16)) ? __ldg(src + x) : 0u;
+        pre[i] = (valid && x < len && !(upper_zero && i >= 16)) ? __ldg(src + x) : 0u;
       }
     } else {
 #pragma unroll
@@ -184,7 +187,7 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
         const int idx = tid + u * G::THREADS;
         const int t2 = idx >> LOGN, x = idx & (G::N - 1);
         const long long e = grp * G::TPC + t2;
-        pre[u] = (e < jn && x < a.len) ? __ldg(in + e * jstride + x) : 0u;
+        pre[u] = (e < jn && x < len) ? __ldg(in + e * jstride + x) : 0u;
       }
     }
   };
@@ -210,8 +213,9 @@ __global__ void __launch_bounds__(Geo<LOGN, TPCX>::THREADS, min_blocks<Geo<LOGN,
     const long long nxt = grp + gridDim.x;
     constexpr bool kPrefetch = G::THREADS <= 512;  // 32 extra registers
     if (kPrefetch && nxt < groups) load_group(nxt);  // in flight during the passes
-    fwd_passes<LOGN, TPCX>(v, smt, tws, pc, lt, upper_zero);
     const bool second = grp >= groups1;
+    fwd_passes<LOGN, TPCX>(v, smt, tws, pc, lt,
+                           G::NPASS > 1 && (second ? len2 : len1) <= G::N / 2);
     uint32_t* out = second ? out2 : out1;
     const long long jn = second ? a.n_entries2 : a.n_entries;
     const long long e0 = (second ? grp - groups1 : grp) * G::TPC, e = e0 + tr;

@@ -594,6 +594,7 @@ int small_batch(long long items, int primes) {
 bool ntt_tma_fwd_ok(int logn, const NttFwdArgs& a) {
   const bool off = option(kOptNttNoTma) != 0;
   if (off || logn < 11 || logn > 13) return false;
+  if (a.len2 > 0 && a.len2 != a.len) return false;  // one length for both batches
   if (a.fold || a.in64 || a.reduce || a.natural || a.pm) return false;
   const int pl = a.pblk_log ? a.pblk_log : 5;
   if (pl != 5 && pl != 2) return false;

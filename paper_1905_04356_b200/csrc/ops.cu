@@ -307,9 +307,13 @@ int cyclic_product(Context& cx, uint64_t p, int m, int k, int n, MatRef A, MatRe
   } else if (b_cached) {
     StageTimer t_(cx, "ntt_fwd_A");
     FPM_TRY(launch_ntt_fwd(logn, fa, ps, st));
-  } else if (fa.len == fb.len && fa.in64 == fb.in64 && fa.fold == fb.fold &&
-             fa.reduce == fb.reduce && ntt_persist_fwd_ok(logn, fa)) {
+  } else if (fa.in64 == fb.in64 && fa.fold == fb.fold && fa.reduce == fb.reduce &&
+             ntt_persist_fwd_ok(logn, fa) &&
+             (fa.len == fb.len || logn <= 10)) {
+    // short transforms are latency-bound: operands of different lengths (a
+    // middle product) share the launch as well
     NttFwdArgs fab = fa;
+    fab.len2 = fb.len;
     fab.in2 = fb.in; fab.in2_stride = fb.in_stride; fab.in2_prime_stride = fb.in_prime_stride;
     fab.n_entries2 = fb.n_entries; fab.out2 = fb.out; fab.out2_prime_stride = fb.out_prime_stride;
     StageTimer t_(cx, "ntt_fwd_AB");
