@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_1905_04356_b200 import dense  # noqa: E402
+from paper_1905_04356_b200 import _lib, dense  # noqa: E402
 
 
 def main():
@@ -21,6 +21,7 @@ def main():
     F = bench.make_inputs(cfg, "cuda", 4)[0]
     ref = None
     for T in [int(x) for x in os.environ.get('PMB_TS', '16,8,4,2').split(',')]:
+        _lib.set_option("pmbasis_leaf", T)  # the cap of the device leaf order
         dense.pmbasis_dense(F, sigma, [0] * cfg["m"], cfg["p"], T=T)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
