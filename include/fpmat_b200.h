@@ -202,7 +202,7 @@ int fpm_polmat_eval_points(fpm_context* ctx, uint64_t p, int elem_bytes, const v
  * is read).  Defaults are the product configuration; name NULL resets all.
  * Names: no_pdl, host_blocks, no_chirp, ntt_generic, ntt_no_tma,
  * ntt_no_small, ntt_pm_lsu, ntt_pm_scatter, pmbasis_leaf, pmbasis_host_sync,
- * ntt_no_mma, tc_no_pair, tc_pair1, ntt_mma_r16.
+ * ntt_no_mma, tc_no_pair, tc_pair1, ntt_mma_r16, tc_narrow.
  * FPM_ERR_INVALID_ARGUMENT for an unknown name. */
 int fpm_set_option(const char* name, long long value);
 

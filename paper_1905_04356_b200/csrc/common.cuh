@@ -157,6 +157,7 @@ enum Option : int {
   kOptTcPair1,            // "tc_pair1": one-SM tc_pair instead of the CTA-pair kernel
   kOptNttMmaR16,          // "ntt_mma_r16": three radix-16 passes (ntt_mma.cu), not two radix-64
   kOptNttMmaDbg,          // "ntt_mma_dbg": timing experiments of ntt_mma64.cu (WRONG results)
+  kOptTcNarrow,           // "tc_narrow": narrowest column block tc_grouped may pick to fill the SMs (0: off)
   kOptCount
 };
 long long option(Option o);

@@ -610,6 +610,17 @@ int persist_impl(const Args& a, const PrimeSet& ps, cudaStream_t st) {
     return ps.count == 1 ? persist_launch<LOGN, true, 1, FWD>(a, ps, st)
                          : persist_launch<LOGN, false, 1, FWD>(a, ps, st);
   }
+  if constexpr (LOGN <= 7) {
+    // a short batch of short transforms (the PM-Basis nodes of order 16 ... 64)
+    // fills a fraction of the SMs at the default 8192 / N transforms per CTA
+    // and is all latency: a quarter of that per CTA spreads it over 4x the SMs
+    constexpr int kSmallTpc = 2048 >> LOGN;
+    long long tr = a.n_entries;
+    if constexpr (FWD) tr += a.n_entries2;
+    if (option(kOptNttNoSmall) == 0 && tr * 2 <= 148LL * (8192 >> LOGN))
+      return ps.count == 1 ? persist_launch<LOGN, true, kSmallTpc, FWD>(a, ps, st)
+                           : persist_launch<LOGN, false, kSmallTpc, FWD>(a, ps, st);
+  }
   if (a.pm) {
     return ps.count == 1 ? persist_launch<LOGN, true, pm_tpc2<LOGN>(), FWD>(a, ps, st)
                          : persist_launch<LOGN, false, pm_tpc2<LOGN>(), FWD>(a, ps, st);

@@ -407,7 +407,7 @@ const OptDef kOptDefs[kOptCount] = {
     {"no_pdl", 0},      {"host_blocks", 0},   {"no_chirp", 0},     {"ntt_generic", 0},
     {"ntt_no_tma", 0},  {"ntt_no_small", 0},  {"ntt_pm_lsu", 0},   {"ntt_pm_scatter", 0},
     {"pmbasis_leaf", 8}, {"pmbasis_host_sync", 0}, {"ntt_no_mma", 0}, {"tc_no_pair", 0}, {"tc_pair1", 0},
-    {"ntt_mma_r16", 0}, {"ntt_mma_dbg", 0},
+    {"ntt_mma_r16", 0}, {"ntt_mma_dbg", 0}, {"tc_narrow", 8},
 };
 std::atomic<long long> g_opt[kOptCount] = {};
 std::atomic<bool> g_opt_init{false};

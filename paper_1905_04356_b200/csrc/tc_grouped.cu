@@ -380,13 +380,24 @@ int launch_tc_grouped(const TcArgs& t, const PrimeSet& ps, cudaStream_t st) {
   a.mp = 16;
   while (a.mp < t.m && a.mp < 128) a.mp <<= 1;
   a.G = 128 / a.mp;
-  a.mtiles = (t.m + 127) / 128;  // > 1 only with mp = 128, G = 1
   // NB: power of two in [8, 64], <= mp so G accumulators of 4 NB columns fit TMEM
   int nb = 8;
   while (nb < t.n && nb < 64) nb <<= 1;
   if (nb > a.mp) nb = a.mp;
-  a.nblk = (t.n + nb - 1) / nb;
   a.ngroups = (t.npts + a.G - 1) / a.G;
+  a.mtiles = (t.m + 127) / 128;
+  {
+    // few evaluation points (the PM-Basis nodes of order 16 ... 128): one item
+    // per CTA is all latency (B build, MMAs and epilogue of the whole column
+    // block in sequence), so narrower column blocks spread it over more SMs
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int narrow = (int)option(kOptTcNarrow);
+    while (narrow && nb > narrow &&
+           (long long)ps.count * a.ngroups * a.mtiles * ((t.n + nb - 1) / nb) * 2 <= sms)
+      nb >>= 1;
+  }
+  a.nblk = (t.n + nb - 1) / nb;
   a.nch = (t.k + 31) / 32;
   const uint32_t tileB = (uint32_t)(nb / 2) * kSboB;
   a.nring = (int)(kRing / tileB);
