@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   extern __shared__ __align__(16) unsigned char smraw[];
   const int m = a.m, n = a.n, T = a.T;
   const int tid = threadIdx.x;
+  if (a.trace && tid == 0) a.trace[63 * 8] = clock64();  // kernel start (after the dependency wait)
   const F31 f = a.f;
   const uint32_t p = f.p;
   const size_t mn = (size_t)m * n;
@@ -441,9 +442,30 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   const int hw = tid >> 4, l16 = tid & 15;  // half-warp per row
   constexpr int kRowsPerPass = kStepThreads / 16;
 
-  for (int e = tid; e < (int)mn; e += kStepThreads) {
-    const uint32_t* fe = a.F + (long long)e * a.fs;
-    for (int t = 0; t < T; ++t) G[(size_t)t * mn + e] = t < a.lf ? fe[(long long)t * a.ts] : 0u;
+  // the residual list G = F mod x^T: every load of two entries is issued before
+  // the first store.  (The whole prologue -- this load, the barrier setup and
+  // the first ranking -- is 9.3 K cycles of a 228 K-cycle leaf, tools/mbasis_trace.py.)
+  for (int e0 = tid; e0 < (int)mn; e0 += 2 * kStepThreads) {
+    for (int t0 = 0; t0 < T; t0 += 8) {
+      uint32_t v[2][8];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int e = e0 + j * kStepThreads;
+        const uint32_t* fe = a.F + (long long)e * a.fs;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u;
+          v[j][u] = (e < (int)mn && t < T && t < a.lf) ? __ldg(fe + (long long)t * a.ts) : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int e = e0 + j * kStepThreads;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (e < (int)mn && t0 + u < T) G[(size_t)(t0 + u) * mn + e] = v[j][u];
+      }
+    }
   }
   for (int i = tid; i < m; i += kStepThreads) {
     sft[i] = a.s[i];
@@ -867,6 +889,7 @@ __global__ void __launch_bounds__(kStepThreads, 1) mbasis_steps_kernel(const __g
   for (int i = tid; i < m; i += kStepThreads) a.sft_out[i] = sft[i];
   __syncthreads();
   if (tid == 0) flag_release(a.flags + T, a.epoch);
+  if (a.trace && tid == 0) a.trace[63 * 8 + 1] = clock64();  // kernel end
 }
 
 struct BuildArgs {

@@ -35,7 +35,12 @@ def main():
         else:
             d = [r[1] - r[0], 0, 0]
         d += [r[2] - r[1], r[3] - r[2], r[4] - r[3], nxt - r[4]]
-        print(f"{k:4d} " + " ".join(f"{x:10d}" for x in d))
+        print(f"{k:4d} " + " ".join(f"{x:10d}" for x in d) + f"   (solve end -> record start {r[1] - r[5]})")
+    t0, t1 = buf[63 * 8], buf[63 * 8 + 1]
+    T = int(os.environ.get("LEAF_T", "16"))
+    if t0 and t1:
+        print(f"kernel {t1 - t0} cycles: start -> step 0 ranked {buf[0] - t0}, "
+              f"last step end -> kernel end {t1 - buf[(T - 1) * 8 + 4]}")
 
 
 if __name__ == "__main__":
