@@ -31,6 +31,37 @@ def test_reference_arm_line():
     assert d["cpu_baseline"]["cpu"]["model"]
 
 
+def test_reference_arm_under_torchrun():
+    """Launched as the driver launches N > 1 (torch.distributed.run, one process
+    per rank): rank 0 alone times the CPU port and prints the one line, the
+    other ranks exit 0 without work."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+         "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--config",
+         "cfg2"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+    sys.path.insert(0, ROOT)
+    import argparse
+
+    import bench
+
+    # the same config object (incl. the split it names) as the device arm at N = 2
+    assert d["config"] == bench.bench_config(argparse.Namespace(config="cfg2"),
+                                             bench.CONFIGS["cfg2"], 2)
+    assert d["scaling"] == "strong" and "2" in d["config"]["parallelism"]
+
+
 def test_both_arms_print_the_same_config():
     """The reference arm and the device arm build one config object."""
     sys.path.insert(0, ROOT)
