@@ -707,13 +707,22 @@ def main():
 
     import torch
 
+    # one rank per GPU; FPM_BENCH_SMOKE_BACKEND=gloo (functional smoke test of
+    # the N > 1 path on a box with fewer GPUs than ranks, never a measurement)
+    # lets ranks share a device: the split has no data-path collective
+    smoke_backend = os.environ.get("FPM_BENCH_SMOKE_BACKEND")
+    if smoke_backend:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        if smoke_backend:
+            dist.init_process_group(smoke_backend)
+        else:
+            dist.init_process_group("nccl", device_id=device)
 
     from paper_1905_04356_b200 import _lib
 
@@ -776,7 +785,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if mode == "2d" and not args.no_extras:
+    if mode == "2d" and not args.no_extras and not smoke_backend:
         # the optional exchange: one all_gather of the C blocks (NCCL) for a
         # consumer that needs all of C on every rank (not in the timed steps)
         from paper_1905_04356_b200.parallel import gather_blocks
